@@ -1,0 +1,104 @@
+/* tatn_b200.h — C ABI of the B200 (sm_100a) FlashAttention hot path.
+ *
+ * This is the drop-in boundary for the reference's tiled engine
+ * (reference proj/core/include/tatn/flash.hpp:43-73):
+ *
+ *   tatn_fwd  replaces the body of  tatn::flash_forward      (flash.hpp:49-51)
+ *                              and  tatn::blocksparse_forward (flash.hpp:64-67)
+ *   tatn_bwd  replaces the body of  tatn::flash_backward      (flash.hpp:58-59)
+ *                              and  tatn::blocksparse_backward(flash.hpp:71-73)
+ *
+ * The reference computes one head per call on row-major n x d fp64 matrices
+ * (SPEC.md:185). This ABI batches B x H independent heads per call on 16-bit
+ * device buffers (row-major in d, arbitrary b/h/n strides), which is how the
+ * C++ wrapper (tatn::flash_forward in csrc/dropin) and the bench call it.
+ *
+ * Conventions (mirroring the reference's exception classes, flash.hpp:47-48):
+ *   - every entry point returns a tatn_status; no exceptions cross the ABI;
+ *   - no allocation and no host synchronisation on the hot path; the caller
+ *     provides device buffers and (for the backward) a workspace;
+ *   - stream-ordered on the caller's stream (a cudaStream_t passed as void*);
+ *   - there is no CPU fallback: without an sm_100 device every compute entry
+ *     point returns TATN_E_CUDA.
+ */
+#ifndef TATN_B200_H_
+#define TATN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TATN_B200_ABI_VERSION 1
+
+typedef enum {
+  TATN_OK = 0,
+  TATN_E_ARG = 1,          /* null pointer / malformed descriptor        (std::invalid_argument) */
+  TATN_E_SHAPE = 2,        /* B,H,N,d or stride mismatch                 (std::invalid_argument) */
+  TATN_E_MASK = 3,         /* block-mask size / plan mismatch            (std::invalid_argument) */
+  TATN_E_UNSUPPORTED = 4,  /* valid for the reference, not on this path  (e.g. p_drop != 0)     */
+  TATN_E_CUDA = 5,         /* CUDA runtime / launch failure or no sm_100 device                 */
+  TATN_E_WORKSPACE = 6     /* workspace too small                                                */
+} tatn_status;
+
+typedef enum { TATN_DTYPE_BF16 = 0, TATN_DTYPE_FP16 = 1 } tatn_dtype;
+
+/* tatn::MaskKind (attn_config.hpp:12). Causal masks key j > query i;
+ * KeyPadding masks key j >= valid_len[b] (attn_config.cpp:20-32). Custom n x n
+ * masks are not on the device path (TATN_E_UNSUPPORTED). */
+typedef enum { TATN_MASK_NONE = 0, TATN_MASK_CAUSAL = 1, TATN_MASK_KEY_PADDING = 2 } tatn_mask_kind;
+
+typedef struct {
+  int32_t B, H;      /* independent (batch, head) slices                          */
+  int32_t Nq, Nk;    /* query rows, key rows (Nk <= Nq: key prefix, reference.hpp:43-46) */
+  int32_t d;         /* head dimension: 64 or 128                                 */
+  int32_t dtype;     /* tatn_dtype                                                */
+  /* element strides of the b, h, n dimensions; d is contiguous (stride 1).
+   * dO uses o_str; dQ/dK/dV use q_str/k_str/v_str. Strides must be multiples of 8. */
+  int64_t q_str[3], k_str[3], v_str[3], o_str[3];
+  float tau;               /* softmax scale, finite and > 0 (attn_config.cpp:52)        */
+  int32_t mask_kind;       /* tatn_mask_kind                                            */
+  const int32_t* valid_len;/* device [B] for KEY_PADDING, else NULL                    */
+  /* Block-sparse mode (tatn::BlockMask, block_mask.hpp:14-24): row-major u8 tr x tc
+   * grid in DEVICE memory, or NULL for dense. br, bc must both be 128 and
+   * tr = ceil(Nq/128), tc = ceil(Nk/128). In dense mode tr/tc may be 0. */
+  const uint8_t* block_grid;
+  int32_t br, bc, tr, tc;
+  /* optional device bitmap of tr*tc bits (bit = i*tc + j), OR-ed with the tiles
+   * the kernels actually computed; must be zeroed by the caller. NULL = off. */
+  uint32_t* visited_bitmap;
+  float p_drop;            /* must be 0 (dropout not on this path) -> else UNSUPPORTED   */
+  uint64_t seed;
+} tatn_attn_desc;
+
+/* Host-only descriptor check (no device access); same codes as the compute calls. */
+int tatn_validate(const tatn_attn_desc* desc);
+
+/* Forward: o = softmax(mask(tau q k^T)) v, lse = natural-log logsumexp per row
+ * ([B, H, Nq] contiguous fp32; -inf and o = 0 for fully masked rows). */
+int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, void* o,
+             float* lse, void* stream);
+
+/* Workspace for tatn_bwd: fp32 dQ accumulator [B,H,Nq,d] + D vector [B,H,Nq]. */
+size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc);
+
+/* Backward with recomputation from lse (Algorithm 4).
+ * Writes dq, dk, dv (same dtype/strides as q, k, v). Keys covered by no
+ * visited tile get exactly zero dK/dV (flash.hpp:70). */
+int tatn_bwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v,
+             const void* o, const void* dO, const float* lse, void* dq, void* dk, void* dv,
+             void* workspace, size_t workspace_bytes, void* stream);
+
+const char* tatn_strerror(int status);
+int tatn_abi_version(void);
+
+/* Number of device kernels the last tatn_fwd / tatn_bwd call on this thread launched. */
+int tatn_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TATN_B200_H_ */

@@ -1,0 +1,113 @@
+"""ctypes binding of the C ABI declared in include/tatn_b200.h.
+
+The shared library ``paper_2205_14135_b200/lib/libtatn_b200.so`` is built
+in-tree by ``__graft_entry__.build()`` (or ``make -C paper_2205_14135_b200``).
+There is no fallback: if the library is missing this module raises on import
+of any compute entry point.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libtatn_b200.so"
+
+TATN_OK = 0
+TATN_E_ARG = 1
+TATN_E_SHAPE = 2
+TATN_E_MASK = 3
+TATN_E_UNSUPPORTED = 4
+TATN_E_CUDA = 5
+TATN_E_WORKSPACE = 6
+
+TATN_DTYPE_BF16 = 0
+TATN_DTYPE_FP16 = 1
+
+TATN_MASK_NONE = 0
+TATN_MASK_CAUSAL = 1
+TATN_MASK_KEY_PADDING = 2
+
+# every symbol include/tatn_b200.h declares (checked by tests/test_capi_symbols.py)
+EXPORTED_SYMBOLS = (
+    "tatn_validate",
+    "tatn_fwd",
+    "tatn_bwd_workspace_bytes",
+    "tatn_bwd",
+    "tatn_strerror",
+    "tatn_abi_version",
+    "tatn_last_launch_count",
+)
+
+
+class TatnAttnDesc(ctypes.Structure):
+    """Mirror of ``tatn_attn_desc`` (include/tatn_b200.h)."""
+
+    _fields_ = [
+        ("B", ctypes.c_int32),
+        ("H", ctypes.c_int32),
+        ("Nq", ctypes.c_int32),
+        ("Nk", ctypes.c_int32),
+        ("d", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("q_str", ctypes.c_int64 * 3),
+        ("k_str", ctypes.c_int64 * 3),
+        ("v_str", ctypes.c_int64 * 3),
+        ("o_str", ctypes.c_int64 * 3),
+        ("tau", ctypes.c_float),
+        ("mask_kind", ctypes.c_int32),
+        ("valid_len", ctypes.c_void_p),
+        ("block_grid", ctypes.c_void_p),
+        ("br", ctypes.c_int32),
+        ("bc", ctypes.c_int32),
+        ("tr", ctypes.c_int32),
+        ("tc", ctypes.c_int32),
+        ("visited_bitmap", ctypes.c_void_p),
+        ("p_drop", ctypes.c_float),
+        ("seed", ctypes.c_uint64),
+    ]
+
+
+class TatnError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {strerror(status)} (status {status})")
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the C-ABI library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the attention path)"
+        )
+    lib = ctypes.CDLL(os.fspath(LIB_PATH))
+    vp = ctypes.c_void_p
+    pd = ctypes.POINTER(TatnAttnDesc)
+    lib.tatn_validate.argtypes = [pd]
+    lib.tatn_validate.restype = ctypes.c_int
+    lib.tatn_fwd.argtypes = [pd, vp, vp, vp, vp, vp, vp]
+    lib.tatn_fwd.restype = ctypes.c_int
+    lib.tatn_bwd_workspace_bytes.argtypes = [pd]
+    lib.tatn_bwd_workspace_bytes.restype = ctypes.c_size_t
+    lib.tatn_bwd.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.tatn_bwd.restype = ctypes.c_int
+    lib.tatn_strerror.argtypes = [ctypes.c_int]
+    lib.tatn_strerror.restype = ctypes.c_char_p
+    lib.tatn_abi_version.argtypes = []
+    lib.tatn_abi_version.restype = ctypes.c_int
+    lib.tatn_last_launch_count.argtypes = []
+    lib.tatn_last_launch_count.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def strerror(status: int) -> str:
+    return load().tatn_strerror(status).decode()

@@ -1,0 +1,143 @@
+"""Device-side batched API over the C ABI (torch tensors as device buffers).
+
+This is the "batched device API" of SURVEY.md §8(b)(ii): the bench and the GPU
+parity tests call it; it only packs a ``tatn_attn_desc`` and passes raw device
+pointers plus the current CUDA stream to ``libtatn_b200.so``. PyTorch provides
+memory and streams only — no attention math happens here.
+
+Tensor layout: ``[B, H, N, d]`` with ``d`` contiguous (any b/h/n strides that
+are multiples of 8 elements), dtype bf16 or fp16, on an sm_100 device.
+LSE is ``[B, H, Nq]`` fp32 (natural log).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib
+
+MASK_KINDS = {
+    "none": _lib.TATN_MASK_NONE,
+    "causal": _lib.TATN_MASK_CAUSAL,
+    "key_padding": _lib.TATN_MASK_KEY_PADDING,
+}
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.TATN_DTYPE_BF16
+    if t.dtype == torch.float16:
+        return _lib.TATN_DTYPE_FP16
+    raise TypeError(f"unsupported dtype {t.dtype}: the sm_100a path takes bf16 or fp16")
+
+
+def _strides(t: torch.Tensor, name: str):
+    if t.dim() != 4:
+        raise ValueError(f"{name} must be [B, H, N, d], got shape {tuple(t.shape)}")
+    if t.stride(3) != 1:
+        raise ValueError(f"{name} must be contiguous in d")
+    return (t.stride(0), t.stride(1), t.stride(2))
+
+
+@dataclass
+class AttnSpec:
+    tau: Optional[float] = None
+    mask: str = "none"
+    valid_len: Optional[torch.Tensor] = None  # int32 [B] on device (key_padding)
+    block_grid: Optional[torch.Tensor] = None  # uint8 [tr, tc] on device, 128x128 blocks
+    visited: Optional[torch.Tensor] = None  # int32 [ceil(tr*tc/32)] on device, zeroed by caller
+
+
+def make_desc(q, k, v, o, spec: AttnSpec) -> _lib.TatnAttnDesc:
+    B, H, Nq, d = q.shape
+    Nk = k.shape[2]
+    desc = _lib.TatnAttnDesc()
+    desc.B, desc.H, desc.Nq, desc.Nk, desc.d = B, H, Nq, Nk, d
+    desc.dtype = _dtype_code(q)
+    for t in (k, v, o):
+        if t.dtype != q.dtype:
+            raise TypeError("q, k, v, o must share one dtype")
+    desc.q_str[:] = _strides(q, "q")
+    desc.k_str[:] = _strides(k, "k")
+    desc.v_str[:] = _strides(v, "v")
+    desc.o_str[:] = _strides(o, "o")
+    desc.tau = float(spec.tau) if spec.tau is not None else 1.0 / math.sqrt(d)
+    if spec.mask not in MASK_KINDS:
+        raise ValueError(f"unknown mask kind {spec.mask!r}")
+    desc.mask_kind = MASK_KINDS[spec.mask]
+    desc.valid_len = spec.valid_len.data_ptr() if spec.valid_len is not None else None
+    tr, tc = (Nq + 127) // 128, (Nk + 127) // 128
+    if spec.block_grid is not None:
+        desc.block_grid = spec.block_grid.data_ptr()
+        desc.br = desc.bc = 128
+        desc.tr, desc.tc = spec.block_grid.shape
+    else:
+        desc.block_grid = None
+        desc.tr, desc.tc = tr, tc
+    desc.visited_bitmap = spec.visited.data_ptr() if spec.visited is not None else None
+    desc.p_drop = 0.0
+    desc.seed = 0
+    return desc
+
+
+def _check(status: int, what: str):
+    if status != _lib.TATN_OK:
+        raise _lib.TatnError(status, what)
+
+
+def flash_fwd(q, k, v, spec: Optional[AttnSpec] = None, out=None, lse=None, stream=None):
+    """O, LSE = attention forward (kernel K1) on device tensors."""
+    spec = spec or AttnSpec()
+    lib = _lib.load()
+    B, H, Nq, d = q.shape
+    if out is None:
+        out = torch.empty_like(q, memory_format=torch.contiguous_format)
+    if lse is None:
+        lse = torch.empty((B, H, Nq), dtype=torch.float32, device=q.device)
+    desc = make_desc(q, k, v, out, spec)
+    s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    st = lib.tatn_fwd(ctypes.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                      lse.data_ptr(), s)
+    _check(st, "tatn_fwd")
+    return out, lse
+
+
+def bwd_workspace(q, k, v, spec: Optional[AttnSpec] = None) -> torch.Tensor:
+    spec = spec or AttnSpec()
+    lib = _lib.load()
+    desc = make_desc(q, k, v, q, spec)
+    n = lib.tatn_bwd_workspace_bytes(ctypes.byref(desc))
+    if n == 0:
+        _check(lib.tatn_validate(ctypes.byref(desc)), "tatn_bwd_workspace_bytes")
+    return torch.empty(n, dtype=torch.uint8, device=q.device)
+
+
+def flash_bwd(q, k, v, o, dO, lse, spec: Optional[AttnSpec] = None, dq=None, dk=None, dv=None,
+              workspace=None, stream=None):
+    """dQ, dK, dV = attention backward (kernels K2-K4) on device tensors."""
+    spec = spec or AttnSpec()
+    lib = _lib.load()
+    if dO.stride() != o.stride():
+        dO = dO.contiguous() if o.is_contiguous() else dO.as_strided(o.shape, o.stride())
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    if dq.stride() != q.stride() or dk.stride() != k.stride() or dv.stride() != v.stride():
+        raise ValueError("dq/dk/dv must have the strides of q/k/v")
+    desc = make_desc(q, k, v, o, spec)
+    if workspace is None:
+        workspace = bwd_workspace(q, k, v, spec)
+    s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    st = lib.tatn_bwd(ctypes.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                      dO.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                      workspace.data_ptr(), workspace.numel(), s)
+    _check(st, "tatn_bwd")
+    return dq, dk, dv
+
+
+def last_launch_count() -> int:
+    return _lib.load().tatn_last_launch_count()

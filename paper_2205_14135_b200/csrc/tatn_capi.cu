@@ -1,0 +1,188 @@
+// tatn_capi.cu — C-ABI entry points (include/tatn_b200.h): descriptor
+// validation, TMA tensor-map construction and kernel launches.
+//
+// Error behaviour mirrors the reference's exceptions (flash.hpp:47-48,
+// attn_config.cpp:42-58): shape / plan / mask mismatches and invalid tau or
+// p_drop are reported as status codes instead of std::invalid_argument.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/tatn_b200.h"
+#include "tatn_bwd.cuh"
+#include "tatn_fwd.cuh"
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 4-D map over (d, n, h, b) with a 64 x rows box and 128B swizzle.
+bool make_map_4d(CUtensorMap* map, CUtensorMapDataType dt, uint32_t elem_bytes, const void* base, int d, int n,
+                 int H, int B, const int64_t str[3], int box_rows, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                 int box_cols = 64) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(B)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(str[2]) * elem_bytes, static_cast<cuuint64_t>(str[1]) * elem_bytes,
+                           static_cast<cuuint64_t>(str[0]) * elem_bytes};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool strides_ok(const int64_t s[3], int H, int N, int d) {
+  for (int i = 0; i < 3; ++i)
+    if (s[i] <= 0 || (s[i] % 8) != 0) return false;
+  (void)H;
+  (void)N;
+  (void)d;
+  return true;
+}
+
+int validate(const tatn_attn_desc* d) {
+  if (d == nullptr) return TATN_E_ARG;
+  if (d->B < 1 || d->H < 1 || d->Nq < 1 || d->Nk < 1) return TATN_E_SHAPE;
+  if (d->Nk > d->Nq) return TATN_E_SHAPE;  // more keys than n (reference.cpp:25-26)
+  if (d->d != 64 && d->d != 128) return TATN_E_UNSUPPORTED;
+  if (d->dtype != TATN_DTYPE_BF16 && d->dtype != TATN_DTYPE_FP16) return TATN_E_UNSUPPORTED;
+  if (!(d->tau > 0.f) || !std::isfinite(d->tau)) return TATN_E_ARG;  // attn_config.cpp:52
+  if (!(d->p_drop >= 0.f && d->p_drop < 1.f)) return TATN_E_ARG;      // attn_config.cpp:54
+  if (d->p_drop != 0.f) return TATN_E_UNSUPPORTED;
+  if (d->mask_kind != TATN_MASK_NONE && d->mask_kind != TATN_MASK_CAUSAL && d->mask_kind != TATN_MASK_KEY_PADDING)
+    return TATN_E_UNSUPPORTED;
+  if (d->mask_kind == TATN_MASK_KEY_PADDING && d->valid_len == nullptr) return TATN_E_ARG;
+  if (!strides_ok(d->q_str, d->H, d->Nq, d->d) || !strides_ok(d->k_str, d->H, d->Nk, d->d) ||
+      !strides_ok(d->v_str, d->H, d->Nk, d->d) || !strides_ok(d->o_str, d->H, d->Nq, d->d))
+    return TATN_E_SHAPE;
+  const int tr = (d->Nq + 127) / 128, tc = (d->Nk + 127) / 128;
+  if (d->block_grid != nullptr) {
+    if (d->br != 128 || d->bc != 128) return TATN_E_MASK;  // bmask block sizes must equal the plan's
+    if (d->tr != tr || d->tc != tc) return TATN_E_MASK;
+  }
+  if (d->visited_bitmap != nullptr && (d->tr != tr || d->tc != tc)) return TATN_E_MASK;
+  if (d->Nq > (1 << 24) || static_cast<int64_t>(d->B) * d->H > (1ll << 31) - 1) return TATN_E_SHAPE;
+  return TATN_OK;
+}
+
+CUtensorMapDataType tma_dtype(int dtype) {
+  return dtype == TATN_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+}
+
+template <int D, bool BF16>
+cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
+                       const tatn_dev::FwdParams& p, cudaStream_t stream) {
+  using Cfg = tatn_dev::FwdCfg<D>;
+  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16>;
+  static bool attr_set = false;  // benign race: idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid(p.B * p.H, p.n_pairs);
+  kern<<<grid, tatn_dev::kFwdThreads, Cfg::kSmemBytes, stream>>>(q, k, v, o, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int tatn_validate(const tatn_attn_desc* desc) { return validate(desc); }
+
+int tatn_abi_version(void) { return TATN_B200_ABI_VERSION; }
+
+int tatn_last_launch_count(void) { return g_last_launches; }
+
+const char* tatn_strerror(int status) {
+  switch (status) {
+    case TATN_OK: return "ok";
+    case TATN_E_ARG: return "invalid argument";
+    case TATN_E_SHAPE: return "shape or stride mismatch";
+    case TATN_E_MASK: return "block mask / plan mismatch";
+    case TATN_E_UNSUPPORTED: return "unsupported on the sm_100a path";
+    case TATN_E_CUDA: return "CUDA error or no sm_100 device";
+    case TATN_E_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, void* o, float* lse,
+             void* stream) {
+  g_last_launches = 0;
+  int st = validate(desc);
+  if (st != TATN_OK) return st;
+  if (!q || !k || !v || !o || !lse) return TATN_E_ARG;
+  const tatn_attn_desc& d = *desc;
+  const CUtensorMapDataType dt = tma_dtype(d.dtype);
+  CUtensorMap mq, mk, mv, mo;
+  if (!make_map_4d(&mq, dt, 2, q, d.d, d.Nq, d.H, d.B, d.q_str, 128) ||
+      !make_map_4d(&mk, dt, 2, k, d.d, d.Nk, d.H, d.B, d.k_str, 128) ||
+      !make_map_4d(&mv, dt, 2, v, d.d, d.Nk, d.H, d.B, d.v_str, 128) ||
+      !make_map_4d(&mo, dt, 2, o, d.d, d.Nq, d.H, d.B, d.o_str, 128))
+    return TATN_E_CUDA;
+  tatn_dev::FwdParams p{};
+  p.B = d.B;
+  p.H = d.H;
+  p.Nq = d.Nq;
+  p.Nk = d.Nk;
+  p.scale_log2 = d.tau * 1.4426950408889634f;
+  p.mask_kind = d.mask_kind;
+  p.valid_len = d.valid_len;
+  p.grid = d.block_grid;
+  p.tr = (d.Nq + 127) / 128;
+  p.tc = (d.Nk + 127) / 128;
+  p.visited = d.visited_bitmap;
+  p.lse = lse;
+  p.n_pairs = (d.Nq + 255) / 256;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  const bool bf16 = d.dtype == TATN_DTYPE_BF16;
+  if (d.d == 128)
+    e = bf16 ? launch_fwd<128, true>(mq, mk, mv, mo, p, s) : launch_fwd<128, false>(mq, mk, mv, mo, p, s);
+  else
+    e = bf16 ? launch_fwd<64, true>(mq, mk, mv, mo, p, s) : launch_fwd<64, false>(mq, mk, mv, mo, p, s);
+  if (e != cudaSuccess) return TATN_E_CUDA;
+  g_last_launches = 1;
+  return TATN_OK;
+}
+
+size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc) {
+  if (validate(desc) != TATN_OK) return 0;
+  const size_t rows = static_cast<size_t>(desc->B) * desc->H * desc->Nq;
+  return rows * desc->d * sizeof(float) + rows * sizeof(float) + 256;
+}
+
+int tatn_bwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, const void* o, const void* dO,
+             const float* lse, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  int st = validate(desc);
+  if (st != TATN_OK) return st;
+  if (!q || !k || !v || !o || !dO || !lse || !dq || !dk || !dv || !workspace) return TATN_E_ARG;
+  if (workspace_bytes < tatn_bwd_workspace_bytes(desc)) return TATN_E_WORKSPACE;
+  return tatn_bwd_launch(*desc, q, k, v, o, dO, lse, dq, dk, dv, workspace, static_cast<cudaStream_t>(stream),
+                         &g_last_launches);
+}
+
+}  // extern "C"

@@ -1,0 +1,382 @@
+// tatn_fwd.cuh — FlashAttention forward for sm_100a (kernel K1).
+//
+// Replaces the body of tatn::flash_forward / tatn::blocksparse_forward
+// (reference proj/core/include/tatn/flash.hpp:43-67), i.e. Algorithm 2 of the
+// paper without dropout. The reference's loop order is
+// K/V-block outer, Q-block inner with O/l/m read-modify-written to HBM each
+// outer pass; outputs are schedule-invariant (flash.hpp:37-40),
+// so here each CTA owns two 128-row Q tiles and streams K/V tiles through
+// shared memory: O, l, m never leave the SM until the final write.
+//
+// CTA layout (320 threads):
+//   warps 0-3  softmax/correction/epilogue for Q tile A (one TMEM lane per thread)
+//   warps 4-7  same for Q tile B
+//   warp  8    TMA producer (Q once, K/V ring)
+//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (512 cols): S_A [0,128) S_B [128,256) O_A [256,256+D) O_B [256+D, 256+2D);
+// P (bf16/fp16) overwrites the first 64 columns of S_q once S_q is in registers.
+// Per K/V tile t the MMA issues S_q = Q_q K_t^T for both tiles, then
+// O_q += P_q V_t after softmax_q signals P ready; tcgen05 ops from one thread
+// execute in order, so the next S_q write cannot overtake the P_q read.
+#pragma once
+
+#include "sm100_ptx.cuh"
+#include "tatn_params.h"
+
+namespace tatn_dev {
+
+constexpr int kBM = 128;  // query rows per Q tile
+constexpr int kBN = 128;  // keys per K/V tile
+constexpr int kFwdThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;  // lazy O rescale (log2 units)
+
+template <int D>
+struct FwdCfg {
+  static constexpr int kSubs = D / 64;                   // 128B-swizzle column blocks
+  static constexpr int kSubBytes = 128 * 128;            // 128 rows x 128 bytes
+  static constexpr int kTileBytes = kSubs * kSubBytes;   // one 128 x D tile (16-bit)
+  static constexpr int kStages = (D == 128) ? 2 : 4;
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = 2 * kTileBytes;
+  static constexpr int kOffV = kOffK + kStages * kTileBytes;
+  static constexpr int kOffBar = kOffV + kStages * kTileBytes;
+  static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // + alignment slack
+  static constexpr uint32_t kTmemS = 0;
+  static constexpr uint32_t kTmemO = 256;
+};
+
+struct FwdSched {
+  int q0[2];    // first global query row of each tile
+  int nkv[2];   // dense mode: number of leading K/V tiles the tile visits
+  int T;        // union length (tiles 0..T-1 are candidates)
+  int kv_limit; // keys >= kv_limit are masked (Nk, or min(Nk, valid_len[b]))
+  const uint8_t* row[2];
+  bool sparse;
+
+  __device__ __forceinline__ bool member(int q, int t) const {
+    if (sparse) return row[q] != nullptr && row[q][t] != 0;
+    return t < nkv[q];
+  }
+};
+
+__device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, int pair) {
+  FwdSched s;
+  s.sparse = p.grid != nullptr;
+  int kv_limit = p.Nk;
+  if (p.mask_kind == kMaskKeyPadding && p.valid_len != nullptr) kv_limit = min(kv_limit, max(p.valid_len[b], 0));
+  s.kv_limit = kv_limit;
+  const int ntiles_kv = (kv_limit + kBN - 1) / kBN;
+  s.T = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int qt = pair * 2 + q;
+    s.q0[q] = qt * kBM;
+    s.row[q] = nullptr;
+    int n = 0;
+    if (s.q0[q] < p.Nq) {
+      if (s.sparse) {
+        s.row[q] = (qt < p.tr) ? p.grid + static_cast<size_t>(qt) * p.tc : nullptr;
+      } else {
+        n = ntiles_kv;
+        if (p.mask_kind == kMaskCausal) n = min(n, (s.q0[q] + kBM - 1) / kBN + 1);
+      }
+    }
+    s.nkv[q] = n;
+  }
+  s.T = s.sparse ? p.tc : max(s.nkv[0], s.nkv[1]);
+  return s;
+}
+
+template <int D, bool BF16>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    tatn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                    const FwdParams p) {
+  using Cfg = FwdCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
+
+  const uint32_t sQ = smem_base + Cfg::kOffQ;
+  const uint32_t sK = smem_base + Cfg::kOffK;
+  const uint32_t sV = smem_base + Cfg::kOffV;
+  const uint32_t bar0 = smem_base + Cfg::kOffBar;
+  // barrier slots (8 bytes each)
+  auto BAR = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
+  const int kBarQ = 0;
+  const int kBarKFull = 1;                       // + stage
+  const int kBarKEmpty = kBarKFull + Cfg::kStages;
+  const int kBarVFull = kBarKEmpty + Cfg::kStages;
+  const int kBarVEmpty = kBarVFull + Cfg::kStages;
+  const int kBarSFull = kBarVEmpty + Cfg::kStages;  // + q
+  const int kBarPFull = kBarSFull + 2;
+  const int kBarOFinal = kBarPFull + 2;
+  const int kNumBars = kBarOFinal + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffBar + 8 * 30);
+
+  const int warp = static_cast<int>(warp_id());
+  const int lane = static_cast<int>(lane_id());
+  const int bh = blockIdx.x;
+  const int b = bh / p.H;
+  const int h = bh - b * p.H;
+  const int pair = (p.mask_kind == kMaskCausal && p.grid == nullptr) ? (p.n_pairs - 1 - static_cast<int>(blockIdx.y))
+                                                                     : static_cast<int>(blockIdx.y);
+
+  if (threadIdx.x == 0) {
+    mbar_init(BAR(kBarQ), 1);
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(BAR(kBarKFull + s), 1);
+      mbar_init(BAR(kBarKEmpty + s), 1);
+      mbar_init(BAR(kBarVFull + s), 1);
+      mbar_init(BAR(kBarVEmpty + s), 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(BAR(kBarSFull + q), 1);
+      mbar_init(BAR(kBarPFull + q), 128);
+      mbar_init(BAR(kBarOFinal + q), 1);
+    }
+    (void)kNumBars;
+    fence_mbar_init();
+  }
+  if (warp == 9) {
+    tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const FwdSched sc = make_fwd_sched(p, b, pair);
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmO);
+      mbar_expect_tx(BAR(kBarQ), 2 * Cfg::kTileBytes);
+      for (int q = 0; q < 2; ++q)
+        for (int s = 0; s < Cfg::kSubs; ++s)
+          tma_load_4d(sQ + q * Cfg::kTileBytes + s * Cfg::kSubBytes, &tmQ, BAR(kBarQ), s * 64, sc.q0[q], h, b);
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < sc.T; ++t) {
+        if (!sc.member(0, t) && !sc.member(1, t)) continue;
+        mbar_wait(BAR(kBarKEmpty + stage), ph ^ 1);
+        mbar_expect_tx(BAR(kBarKFull + stage), Cfg::kTileBytes);
+        for (int s = 0; s < Cfg::kSubs; ++s)
+          tma_load_4d(sK + stage * Cfg::kTileBytes + s * Cfg::kSubBytes, &tmK, BAR(kBarKFull + stage), s * 64,
+                      t * kBN, h, b);
+        mbar_wait(BAR(kBarVEmpty + stage), ph ^ 1);
+        mbar_expect_tx(BAR(kBarVFull + stage), Cfg::kTileBytes);
+        for (int s = 0; s < Cfg::kSubs; ++s)
+          tma_load_4d(sV + stage * Cfg::kTileBytes + s * Cfg::kSubBytes, &tmV, BAR(kBarVFull + stage), s * 64,
+                      t * kBN, h, b);
+        if (++stage == Cfg::kStages) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t ab = BF16 ? 1u : 0u;
+      constexpr uint32_t idesc_qk = make_idesc_f16(ab, 128, kBN, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_f16(ab, 128, D, 0, 1);
+      mbar_wait(BAR(kBarQ), 0);
+      tc_fence_after();
+      uint32_t acc[2] = {0, 0};
+      uint32_t pph[2] = {0, 0};
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < sc.T; ++t) {
+        const bool mem[2] = {sc.member(0, t), sc.member(1, t)};
+        if (!mem[0] && !mem[1]) continue;
+        mbar_wait(BAR(kBarKFull + stage), ph);
+        tc_fence_after();
+        const uint32_t kbase = sK + stage * Cfg::kTileBytes;
+        for (int q = 0; q < 2; ++q) {
+          if (!mem[q]) continue;
+          const uint32_t qbase = sQ + q * Cfg::kTileBytes;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * Cfg::kSubBytes + (kk & 3) * 32;
+            const uint64_t a = make_sdesc_sw128(qbase + off, 16, 1024);
+            const uint64_t bdesc = make_sdesc_sw128(kbase + off, 16, 1024);
+            mma_ss(tmem_base + Cfg::kTmemS + q * 128, a, bdesc, idesc_qk, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(BAR(kBarSFull + q));
+          if (p.visited != nullptr) {
+            const int qt = pair * 2 + q;
+            const long long bit = static_cast<long long>(qt) * p.tc + t;
+            atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
+          }
+        }
+        mma_commit(BAR(kBarKEmpty + stage));
+        mbar_wait(BAR(kBarVFull + stage), ph);
+        tc_fence_after();
+        const uint32_t vbase = sV + stage * Cfg::kTileBytes;
+        for (int q = 0; q < 2; ++q) {
+          if (!mem[q]) continue;
+          mbar_wait(BAR(kBarPFull + q), pph[q]);
+          pph[q] ^= 1;
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            // V tile is MN-major for this product: 16 keys = 2 x 1024B swizzle atoms.
+            const uint64_t bdesc = make_sdesc_sw128(vbase + kk * 2048, Cfg::kSubBytes, 1024);
+            mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemS + q * 128 + kk * 8, bdesc,
+                   idesc_pv, (acc[q] | (kk > 0 ? 1u : 0u)));
+          }
+          acc[q] = 1;
+        }
+        mma_commit(BAR(kBarVEmpty + stage));
+        if (++stage == Cfg::kStages) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+      mma_commit(BAR(kBarOFinal + 0));
+      mma_commit(BAR(kBarOFinal + 1));
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int q = warp >> 2;               // Q tile of this warpgroup
+    const int wq = warp & 3;               // TMEM lane quadrant
+    const int row = wq * 32 + lane;        // row within the tile == TMEM lane
+    const int grow = sc.q0[q] + row;       // global query row
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t tS = tmem_base + lane_off + Cfg::kTmemS + q * 128;
+    const uint32_t tO = tmem_base + lane_off + Cfg::kTmemO + q * D;
+    const float sl2 = p.scale_log2;
+    const bool causal = p.mask_kind == kMaskCausal;
+
+    float m_run = -INFINITY;  // running max of tau*s*log2(e), possibly stale by <= threshold
+    float l_run = 0.f;        // running denominator relative to m_run
+    int n_done = 0;
+    uint32_t sph = 0;
+
+    for (int t = 0; t < sc.T; ++t) {
+      if (!sc.member(q, t)) continue;
+      mbar_wait(BAR(kBarSFull + q), sph);
+      sph ^= 1;
+      tc_fence_after();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+
+      const int k0 = t * kBN;
+      const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > sc.q0[q]);
+      if (need_mask) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          const int kj = k0 + i;
+          const bool masked = (kj >= sc.kv_limit) || (causal && kj > grow);
+          if (masked) sr[i] = __float_as_uint(-INFINITY);
+        }
+      }
+      float mx0 = __uint_as_float(sr[0]), mx1 = __uint_as_float(sr[1]);
+      float mx2 = __uint_as_float(sr[2]), mx3 = __uint_as_float(sr[3]);
+#pragma unroll
+      for (int i = 4; i < 128; i += 4) {
+        mx0 = fmaxf(mx0, __uint_as_float(sr[i]));
+        mx1 = fmaxf(mx1, __uint_as_float(sr[i + 1]));
+        mx2 = fmaxf(mx2, __uint_as_float(sr[i + 2]));
+        mx3 = fmaxf(mx3, __uint_as_float(sr[i + 3]));
+      }
+      const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      float alpha = 1.f;
+      if (m_tile - m_run > kRescaleThreshold) {  // false for NaN (both -inf)
+        alpha = ex2_approx(m_run - m_tile);      // 0 when m_run == -inf
+        m_run = m_tile;
+      }
+      l_run *= alpha;
+      const bool rescale = (n_done > 0) && (alpha != 1.f);
+      if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c * 32, o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tO + c * 32, o);
+        }
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      float rs0 = 0.f, rs1 = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float p0 = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), sl2, -m_use));
+        const float p1 = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), sl2, -m_use));
+        rs0 += p0;
+        rs1 += p1;
+        pk[i] = pack2<BF16>(p0, p1);
+      }
+      l_run += rs0 + rs1;
+      tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(BAR(kBarPFull + q));
+      ++n_done;
+    }
+
+    // ------------------------------------------------------------ epilogue
+    if (sc.q0[q] < p.Nq) {
+      mbar_wait(BAR(kBarQ), 0);  // Q_q smem is reused as the O staging buffer
+      const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
+      const uint32_t sO = sQ + q * Cfg::kTileBytes;
+      if (n_done > 0) {
+        mbar_wait(BAR(kBarOFinal + q), 0);
+        tc_fence_after();
+      }
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        if (n_done > 0) {
+          tmem_ld32(tO + c * 32, o);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = 0u;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack2<BF16>(__uint_as_float(o[2 * i]) * inv_l, __uint_as_float(o[2 * i + 1]) * inv_l);
+        const int sub = (c * 32) / 64;
+        const int chunk0 = ((c * 32) % 64) / 8;
+        const uint32_t rbase = sO + sub * Cfg::kSubBytes + row * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t addr = rbase + (((chunk0 + j) ^ (row & 7)) << 4);
+          st_shared_v4(addr, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+      }
+      if (grow < p.Nq) {
+        const float lse = (l_run > 0.f) ? (m_run + __log2f(l_run)) * 0.69314718055994530942f : -INFINITY;
+        p.lse[static_cast<size_t>(bh) * p.Nq + grow] = lse;
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1 + q, 128);
+      if (row == 0) {
+        for (int s = 0; s < Cfg::kSubs; ++s) tma_store_4d(&tmO, sO + s * Cfg::kSubBytes, s * 64, sc.q0[q], h, b);
+        bulk_commit();
+        bulk_wait_read_all();
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace tatn_dev

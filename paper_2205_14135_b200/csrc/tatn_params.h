@@ -1,0 +1,39 @@
+// tatn_params.h — kernel parameter blocks shared by the host launcher
+// (tatn_capi.cu) and the device kernels. Plain-old-data only.
+#pragma once
+#include <cstdint>
+
+namespace tatn_dev {
+
+// Mirrors tatn::MaskKind (reference attn_config.hpp:12) for the kinds the
+// device path implements. Custom (n x n additive) masks are not on the path.
+enum MaskKindDev : int { kMaskNone = 0, kMaskCausal = 1, kMaskKeyPadding = 2 };
+
+struct FwdParams {
+  int B, H, Nq, Nk;
+  float scale_log2;          // tau * log2(e): scores are kept in the log2 domain
+  int mask_kind;             // MaskKindDev
+  const int32_t* valid_len;  // [B] (KeyPadding) or nullptr
+  const uint8_t* grid;       // block-sparse grid tr x tc at 128x128 tiles, or nullptr (dense)
+  int tr, tc;                // tile counts (always set; grid dims when grid != nullptr)
+  uint32_t* visited;         // optional tr*tc bitmap of tiles the kernel computed
+  float* lse;                // [B, H, Nq] natural-log logsumexp (fp32)
+  int n_pairs;               // ceil(Nq / 256): CTAs per (b, h)
+};
+
+struct BwdParams {
+  int B, H, Nq, Nk;
+  float scale_log2;  // tau * log2(e)
+  float tau;
+  int mask_kind;
+  const int32_t* valid_len;
+  const uint8_t* grid;
+  int tr, tc;
+  uint32_t* visited;
+  const float* lse;  // [B, H, Nq]
+  float* delta;      // [B, H, Nq] workspace: D_i = rowsum(dO_i * O_i)
+  float* dq_acc;     // [B, H, Nq, d] fp32 workspace
+  int n_ktiles;      // ceil(Nk / 128)
+};
+
+}  // namespace tatn_dev
