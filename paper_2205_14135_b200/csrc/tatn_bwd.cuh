@@ -1,10 +1,623 @@
-// tatn_bwd.cuh — placeholder until the backward kernels land.
+// tatn_bwd.cuh — FlashAttention backward for sm_100a (kernels K2, K3, K4).
+//
+// Replaces the body of tatn::flash_backward / tatn::blocksparse_backward
+// (reference flash.hpp:53-73), i.e. Algorithm 4 without
+// dropout: P is recomputed per tile from the saved logsumexp, D_i =
+// rowsum(dO_i * O_i) (reference.cpp:287-290), dS = P * (dP - D),
+// dV = P^T dO, dK = tau dS^T Q, dQ = tau dS K. As in Alg 4 the K/V block is
+// the outer loop (one CTA per 128-key tile) and dQ is a read-modify-write
+// accumulation — here an fp32 bulk reduce-add into an L2-resident workspace.
+//
+//   K2 tatn_bwd_pre   : D_i, lse2_i = LSE_i*log2(e) (+inf for empty/padded rows), zero dQacc
+//   K3 tatn_bwd_kernel: per (b, h, key tile) loop over 64-row Q tiles
+//   K4 tatn_bwd_post  : dQ = bf16/fp16(dQacc)
+//
+// K3 CTA layout (320 threads):
+//   warps 0-3 "softmax": thread = key row (TMEM lane). Recompute P^T, dS^T.
+//   warps 4-7 "dQ":      thread = head-dim row of dQ^T (TMEM lane); stage + bulk reduce.
+//   warp  8   TMA producer (K, V once; Q_i, dO_i, lse2_i, D_i ring)
+//   warp  9   TMEM allocator + tcgen05.mma issuer
+// Per Q tile i the MMA computes (M = 128 keys unless noted)
+//   front: S^T = K Q_i^T, dP^T = V dO_i^T                      (N = 64 queries)
+//   back : dV += P^T dO_i, dK += dS^T Q_i  (A from TMEM)       (N = d)
+//          dQ_i^T = K^T dS^T  (M = d rows used, A/B from SMEM) (N = 64 queries)
+// with two TMEM buffers X0/X1 holding {S^T | dP^T} so that front(i+1)
+// overlaps softmax(i) and back(i) overlaps softmax(i+1).
 #pragma once
+
 #include <cuda_runtime.h>
+
 #include "../../include/tatn_b200.h"
+#include "sm100_ptx.cuh"
 #include "tatn_params.h"
 
-static inline int tatn_bwd_launch(const tatn_attn_desc&, const void*, const void*, const void*, const void*,
-                                  const void*, const float*, void*, void*, void*, void*, cudaStream_t, int*) {
-  return TATN_E_UNSUPPORTED;
+namespace tatn_dev {
+
+constexpr int kBwdThreads = 320;
+constexpr int kBwdQT = 64;    // query rows per Q tile
+constexpr int kBwdKT = 128;   // keys per CTA
+
+template <int D>
+struct BwdCfg {
+  static constexpr int kSubs = D / 64;
+  static constexpr int kKVTile = kSubs * 128 * 128;   // 128 rows x D x 2B
+  static constexpr int kQSub = 64 * 128;              // 64 rows x 128B
+  static constexpr int kQTile = kSubs * kQSub;        // 64 rows x D x 2B
+  static constexpr int kStages = (D == 128) ? 3 : 4;
+  static constexpr int kDSBytes = 128 * 128;          // 128 keys x 64 q x 2B
+  static constexpr int kDQBytes = kBwdQT * D * 4;     // fp32 staging
+  static constexpr int kVecBytes = 2 * kBwdQT * 4;    // lse2 + D
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + kKVTile;
+  static constexpr int kOffQ = kOffV + kKVTile;
+  static constexpr int kOffDO = kOffQ + kStages * kQTile;
+  static constexpr int kOffDS = kOffDO + kStages * kQTile;
+  static constexpr int kOffDQ = kOffDS + 2 * kDSBytes;
+  static constexpr int kOffVec = kOffDQ + kDQBytes;
+  static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
+  static constexpr int kSmemBytes = kOffBar + 256 + 1024;
+  static constexpr uint32_t kTmemX = 0;    // X_x = x*128: S^T [0,64) dP^T [64,128)
+  static constexpr uint32_t kTmemDV = 256;
+  static constexpr uint32_t kTmemDK = 256 + D;
+};
+
+struct BwdSched {
+  int k0;        // first key of the tile
+  int kv_limit;  // keys >= kv_limit are masked
+  int i_begin;   // first candidate Q tile (64 rows)
+  int i_end;     // one past the last candidate Q tile
+  const uint8_t* gcol;  // block-sparse grid column base (grid + j), stride tc; nullptr = dense
+  int tc;
+
+  __device__ __forceinline__ bool member(int i) const {
+    if (gcol == nullptr) return true;
+    return gcol[static_cast<size_t>(i >> 1) * tc] != 0;
+  }
+};
+
+__device__ __forceinline__ BwdSched make_bwd_sched(const BwdParams& p, int b, int j) {
+  BwdSched s;
+  s.k0 = j * kBwdKT;
+  int kv_limit = p.Nk;
+  if (p.mask_kind == kMaskKeyPadding && p.valid_len != nullptr) kv_limit = min(kv_limit, max(p.valid_len[b], 0));
+  s.kv_limit = kv_limit;
+  s.tc = p.tc;
+  const int n_qt = (p.Nq + kBwdQT - 1) / kBwdQT;
+  if (p.grid != nullptr) {
+    s.gcol = p.grid + j;
+    s.i_begin = 0;
+    s.i_end = n_qt;
+  } else {
+    s.gcol = nullptr;
+    s.i_begin = (p.mask_kind == kMaskCausal) ? (s.k0 / kBwdQT) : 0;
+    s.i_end = (s.k0 < kv_limit) ? n_qt : 0;
+  }
+  if (s.i_begin > s.i_end) s.i_begin = s.i_end;
+  return s;
+}
+
+// ---------------------------------------------------------------- K2
+// One 8-element chunk per thread. Rows are padded to a multiple of 128.
+template <int D, bool BF16>
+__global__ void __launch_bounds__(256) tatn_bwd_pre(const uint16_t* __restrict__ o, const uint16_t* __restrict__ dO,
+                                                    const float* __restrict__ lse, int64_t ob, int64_t oh, int64_t on,
+                                                    int B, int H, int Nq, int Nq_pad, float* __restrict__ lse2,
+                                                    float* __restrict__ delta, float* __restrict__ dq_acc) {
+  constexpr int kChunks = D / 8;
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long row = gid / kChunks;  // over B*H*Nq_pad
+  const int c = static_cast<int>(gid % kChunks);
+  const long long total = static_cast<long long>(B) * H * Nq_pad;
+  float part = 0.f;
+  int qi = 0;
+  long long bh = 0;
+  if (row < total) {
+    bh = row / Nq_pad;
+    qi = static_cast<int>(row - bh * Nq_pad);
+    const int b = static_cast<int>(bh / H), h = static_cast<int>(bh % H);
+    if (qi < Nq) {
+      const size_t off = static_cast<size_t>(b) * ob + static_cast<size_t>(h) * oh + static_cast<size_t>(qi) * on + c * 8;
+      const uint4 ov = *reinterpret_cast<const uint4*>(o + off);
+      const uint4 dv = *reinterpret_cast<const uint4*>(dO + off);
+      const uint32_t* ow = reinterpret_cast<const uint32_t*>(&ov);
+      const uint32_t* dw = reinterpret_cast<const uint32_t*>(&dv);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 a, bb;
+        if constexpr (BF16) {
+          a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[k]));
+          bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dw[k]));
+        } else {
+          a = __half22float2(*reinterpret_cast<const __half2*>(&ow[k]));
+          bb = __half22float2(*reinterpret_cast<const __half2*>(&dw[k]));
+        }
+        part = fmaf(a.x, bb.x, part);
+        part = fmaf(a.y, bb.y, part);
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(dq_acc + row * D + c * 8);
+    dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // reduce over the kChunks lanes of this row (kChunks in {8, 16}, aligned within a warp)
+#pragma unroll
+  for (int off = kChunks / 2; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+  if (row < total && c == 0) {
+    delta[row] = part;
+    float l2 = INFINITY;  // P = 0 for padded or fully-masked rows
+    if (qi < Nq) {
+      const float l = lse[bh * Nq + qi];
+      if (l != -INFINITY) l2 = l * 1.4426950408889634f;
+    }
+    lse2[row] = l2;
+  }
+}
+
+// ---------------------------------------------------------------- K4
+template <int D, bool BF16>
+__global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ dq_acc, uint16_t* __restrict__ dq,
+                                                     int64_t qb, int64_t qh, int64_t qn, int B, int H, int Nq,
+                                                     int Nq_pad) {
+  constexpr int kChunks = D / 8;
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long row = gid / kChunks;  // over B*H*Nq
+  const int c = static_cast<int>(gid % kChunks);
+  if (row >= static_cast<long long>(B) * H * Nq) return;
+  const long long bh = row / Nq;
+  const int qi = static_cast<int>(row - bh * Nq);
+  const int b = static_cast<int>(bh / H), h = static_cast<int>(bh % H);
+  const float4* src = reinterpret_cast<const float4*>(dq_acc + (bh * Nq_pad + qi) * D + c * 8);
+  const float4 a = src[0], bb = src[1];
+  uint4 out;
+  out.x = pack2<BF16>(a.x, a.y);
+  out.y = pack2<BF16>(a.z, a.w);
+  out.z = pack2<BF16>(bb.x, bb.y);
+  out.w = pack2<BF16>(bb.z, bb.w);
+  *reinterpret_cast<uint4*>(dq + static_cast<size_t>(b) * qb + static_cast<size_t>(h) * qh +
+                            static_cast<size_t>(qi) * qn + c * 8) = out;
+}
+
+// ---------------------------------------------------------------- K3
+template <int D, bool BF16>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    tatn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                    const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
+                    const BwdParams p, const float* __restrict__ lse2, int Nq_pad) {
+  using Cfg = BwdCfg<D>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
+
+  const uint32_t sK = smem_base + Cfg::kOffK;
+  const uint32_t sV = smem_base + Cfg::kOffV;
+  const uint32_t sQ = smem_base + Cfg::kOffQ;
+  const uint32_t sDO = smem_base + Cfg::kOffDO;
+  const uint32_t sDS = smem_base + Cfg::kOffDS;
+  const uint32_t sDQ = smem_base + Cfg::kOffDQ;
+  const uint32_t sVec = smem_base + Cfg::kOffVec;
+  const float* vec_gen = reinterpret_cast<const float*>(smem_gen + Cfg::kOffVec);
+  const uint32_t bar0 = smem_base + Cfg::kOffBar;
+  auto BAR = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
+  const int kBarKV = 0;
+  const int kBarQFull = 1;
+  const int kBarQEmpty = kBarQFull + S;
+  const int kBarSFull = kBarQEmpty + S;   // [2]
+  const int kBarPFull = kBarSFull + 2;    // [2]
+  const int kBarDQFull = kBarPFull + 2;   // [2]
+  const int kBarDQEmpty = kBarDQFull + 2; // [2]
+  const int kBarDSEmpty = kBarDQEmpty + 2;// [2]
+  const int kBarFinal = kBarDSEmpty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffBar + 8 * 28);
+
+  const int warp = static_cast<int>(warp_id());
+  const int lane = static_cast<int>(lane_id());
+  const int bh = blockIdx.x;
+  const int b = bh / p.H;
+  const int h = bh - b * p.H;
+  const int j = blockIdx.y;  // key tile (j = 0 is the heaviest under a causal mask)
+
+  if (threadIdx.x == 0) {
+    mbar_init(BAR(kBarKV), 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(BAR(kBarQFull + s), 1);
+      mbar_init(BAR(kBarQEmpty + s), 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(BAR(kBarSFull + x), 1);
+      mbar_init(BAR(kBarPFull + x), 128);
+      mbar_init(BAR(kBarDQFull + x), 1);
+      mbar_init(BAR(kBarDQEmpty + x), 128);
+      mbar_init(BAR(kBarDSEmpty + x), 1);
+    }
+    mbar_init(BAR(kBarFinal), 1);
+    fence_mbar_init();
+  }
+  if (warp == 9) {
+    tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const BwdSched sc = make_bwd_sched(p, b, j);
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmDO);
+      mbar_expect_tx(BAR(kBarKV), 2 * Cfg::kKVTile);
+      for (int s = 0; s < Cfg::kSubs; ++s) {
+        tma_load_4d(sK + s * 128 * 128, &tmK, BAR(kBarKV), s * 64, sc.k0, h, b);
+        tma_load_4d(sV + s * 128 * 128, &tmV, BAR(kBarKV), s * 64, sc.k0, h, b);
+      }
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int i = sc.i_begin; i < sc.i_end; ++i) {
+        if (!sc.member(i)) continue;
+        mbar_wait(BAR(kBarQEmpty + stage), ph ^ 1);
+        const uint32_t fb = BAR(kBarQFull + stage);
+        mbar_expect_tx(fb, 2 * Cfg::kQTile + Cfg::kVecBytes);
+        for (int s = 0; s < Cfg::kSubs; ++s) {
+          tma_load_4d(sQ + stage * Cfg::kQTile + s * Cfg::kQSub, &tmQ, fb, s * 64, i * kBwdQT, h, b);
+          tma_load_4d(sDO + stage * Cfg::kQTile + s * Cfg::kQSub, &tmDO, fb, s * 64, i * kBwdQT, h, b);
+        }
+        const float* src = lse2 + static_cast<size_t>(bh) * Nq_pad + i * kBwdQT;
+        const uint32_t vdst = sVec + stage * Cfg::kVecBytes;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(vdst),
+                     "l"(src), "r"(kBwdQT * 4), "r"(fb)
+                     : "memory");
+        const float* srcd = p.delta + static_cast<size_t>(bh) * Nq_pad + i * kBwdQT;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         vdst + kBwdQT * 4),
+                     "l"(srcd), "r"(kBwdQT * 4), "r"(fb)
+                     : "memory");
+        if (++stage == S) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t ab = BF16 ? 1u : 0u;
+      constexpr uint32_t idesc_s = make_idesc_f16(ab, 128, kBwdQT, 0, 0);   // S^T, dP^T
+      constexpr uint32_t idesc_acc = make_idesc_f16(ab, 128, D, 0, 1);      // dV, dK (B MN-major)
+      constexpr uint32_t idesc_dq = make_idesc_f16(ab, 128, kBwdQT, 1, 1);  // dQ^T (A, B MN-major)
+      // list the Q tiles once (the order the producer and consumers use)
+      int n = 0;
+      for (int i = sc.i_begin; i < sc.i_end; ++i) n += sc.member(i) ? 1 : 0;
+      mbar_wait(BAR(kBarKV), 0);
+      tc_fence_after();
+      uint32_t qph[S];
+      for (int s = 0; s < S; ++s) qph[s] = 0;
+      uint32_t pph[2] = {0, 0}, eph[2] = {0, 0};
+
+      auto front_dp = [&](int idx) {
+        const int s = idx % S;
+        const int x = idx & 1;
+        mbar_wait(BAR(kBarQFull + s), qph[s]);
+        qph[s] ^= 1;
+        tc_fence_after();
+        const uint32_t dob = sDO + s * Cfg::kQTile;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t offa = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, make_sdesc_sw128(sV + offa, 16, 1024),
+                 make_sdesc_sw128(dob + offb, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        }
+      };
+      auto front_s = [&](int idx) {
+        const int s = idx % S;
+        const int x = idx & 1;
+        const uint32_t qb = sQ + s * Cfg::kQTile;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t offa = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128, make_sdesc_sw128(sK + offa, 16, 1024),
+                 make_sdesc_sw128(qb + offb, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(BAR(kBarSFull + x));
+      };
+
+      for (int idx = 0; idx < n && idx < 2; ++idx) {
+        front_dp(idx);
+        front_s(idx);
+      }
+      for (int idx = 0; idx < n; ++idx) {
+        const int x = idx & 1;
+        const int s = idx % S;
+        mbar_wait(BAR(kBarPFull + x), pph[x]);
+        pph[x] ^= 1;
+        tc_fence_after();
+        const uint32_t qb = sQ + s * Cfg::kQTile;
+        const uint32_t dob = sDO + s * Cfg::kQTile;
+        const uint32_t accf = idx > 0 ? 1u : 0u;
+        // dV += P^T dO   (P^T bf16 in X_x cols [0,32); dO MN-major, 16 queries per step)
+#pragma unroll
+        for (int kk = 0; kk < kBwdQT / 16; ++kk)
+          mma_ts(tmem_base + Cfg::kTmemDV, tmem_base + Cfg::kTmemX + x * 128 + kk * 8,
+                 make_sdesc_sw128(dob + kk * 2048, Cfg::kQSub, 1024), idesc_acc, accf | (kk > 0 ? 1u : 0u));
+        // dK += dS^T Q   (dS^T bf16 in X_x cols [64,96))
+#pragma unroll
+        for (int kk = 0; kk < kBwdQT / 16; ++kk)
+          mma_ts(tmem_base + Cfg::kTmemDK, tmem_base + Cfg::kTmemX + x * 128 + 64 + kk * 8,
+                 make_sdesc_sw128(qb + kk * 2048, Cfg::kQSub, 1024), idesc_acc, accf | (kk > 0 ? 1u : 0u));
+        // dQ^T = K^T dS^T  (K MN-major as A; dS^T MN-major as B; 16 keys per step) -> X_x cols [0,64)
+        const uint32_t dsb = sDS + (idx & 1) * Cfg::kDSBytes;
+#pragma unroll
+        for (int kk = 0; kk < kBwdKT / 16; ++kk)
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128, make_sdesc_sw128(sK + kk * 2048, 128 * 128, 1024),
+                 make_sdesc_sw128(dsb + kk * 2048, 128 * 128, 1024), idesc_dq, kk > 0 ? 1u : 0u);
+        mma_commit(BAR(kBarDQFull + x));
+        mma_commit(BAR(kBarQEmpty + s));
+        mma_commit(BAR(kBarDSEmpty + (idx & 1)));
+        if (idx + 2 < n) {
+          front_dp(idx + 2);  // dP^T region free: its dS^T was consumed above (in-order)
+          mbar_wait(BAR(kBarDQEmpty + x), eph[x]);  // dQ^T of this tile read out of X_x
+          eph[x] ^= 1;
+          tc_fence_after();
+          front_s(idx + 2);
+        }
+      }
+      mma_commit(BAR(kBarFinal));
+    }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ softmax warpgroup
+    const int r = warp * 32 + lane;  // key row within tile == TMEM lane
+    const int kj = sc.k0 + r;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const float sl2 = p.scale_log2;
+    const float tau = p.tau;
+    const bool causal = p.mask_kind == kMaskCausal;
+    uint32_t sph[2] = {0, 0};
+    uint32_t dsph[2] = {0, 0};
+    uint32_t qph[S];
+    for (int s = 0; s < S; ++s) qph[s] = 0;
+    int idx = 0;
+    for (int i = sc.i_begin; i < sc.i_end; ++i) {
+      if (!sc.member(i)) continue;
+      const int x = idx & 1;
+      const int s = idx % S;
+      if (p.visited != nullptr && r == 0) {
+        const long long bit = static_cast<long long>(i >> 1) * p.tc + j;
+        atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
+      }
+      mbar_wait(BAR(kBarQFull + s), qph[s]);  // lse2 / D vectors landed
+      qph[s] ^= 1;
+      mbar_wait(BAR(kBarSFull + x), sph[x]);
+      sph[x] ^= 1;
+      tc_fence_after();
+      const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + x * 128;
+      uint32_t sr[64], dp[64];
+      tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld32(tX + 64, *reinterpret_cast<uint32_t(*)[32]>(&dp[0]));
+      tmem_ld32(tX + 96, *reinterpret_cast<uint32_t(*)[32]>(&dp[32]));
+      const float* vl = vec_gen + s * (Cfg::kVecBytes / 4);
+      const int i0 = i * kBwdQT;
+      const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0);
+      uint32_t pk[32], dk[32];
+#pragma unroll
+      for (int c2 = 0; c2 < 32; ++c2) {
+        float pv[2], dv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 2 * c2 + e;
+          float pr = ex2_approx(fmaf(__uint_as_float(sr[c]), sl2, -vl[c]));
+          if (need_mask) {
+            const bool masked = (kj >= sc.kv_limit) || (causal && kj > i0 + c);
+            if (masked) pr = 0.f;
+          }
+          pv[e] = pr;
+          dv[e] = pr * (__uint_as_float(dp[c]) - vl[kBwdQT + c]) * tau;
+        }
+        pk[c2] = pack2<BF16>(pv[0], pv[1]);
+        dk[c2] = pack2<BF16>(dv[0], dv[1]);
+      }
+      tmem_st32(tX, pk);        // P^T   -> X_x cols [0,32)
+      tmem_st32(tX + 64, dk);   // dS^T  -> X_x cols [64,96)
+      // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
+      mbar_wait(BAR(kBarDSEmpty + (idx & 1)), dsph[idx & 1] ^ 1);
+      dsph[idx & 1] ^= 1;
+      const uint32_t drow = sDS + (idx & 1) * Cfg::kDSBytes + r * 128;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+        st_shared_v4(drow + ((cc ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+      fence_proxy_async_smem();
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(BAR(kBarPFull + x));
+      ++idx;
+    }
+    // ------------------------------------------------------------ dK / dV epilogue
+    if (idx > 0) {
+      mbar_wait(BAR(kBarFinal), 0);
+      tc_fence_after();
+    } else {
+      mbar_wait(BAR(kBarKV), 0);  // staging reuses K/V smem
+    }
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t tacc = tmem_base + lane_off + (which == 0 ? Cfg::kTmemDK : Cfg::kTmemDV);
+      const uint32_t stg = which == 0 ? sK : sV;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        if (idx > 0) {
+          tmem_ld32(tacc + c * 32, v);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0u;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = pack2<BF16>(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+        const int sub = (c * 32) / 64;
+        const int chunk0 = ((c * 32) % 64) / 8;
+        const uint32_t rb = stg + sub * 128 * 128 + r * 128;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          st_shared_v4(rb + (((chunk0 + e) ^ (r & 7)) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (r == 0) {
+      for (int s = 0; s < Cfg::kSubs; ++s) {
+        tma_store_4d(&tmDK, sK + s * 128 * 128, s * 64, sc.k0, h, b);
+        tma_store_4d(&tmDV, sV + s * 128 * 128, s * 64, sc.k0, h, b);
+      }
+      bulk_commit();
+      bulk_wait_read_all();
+    }
+  } else {
+    // ------------------------------------------------------------ dQ warpgroup
+    const int wq = warp & 3;
+    const int dd = wq * 32 + lane;  // head-dim index == TMEM lane of dQ^T
+    const bool active = dd < D;
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    uint32_t fph[2] = {0, 0};
+    int idx = 0;
+    for (int i = sc.i_begin; i < sc.i_end; ++i) {
+      if (!sc.member(i)) continue;
+      const int x = idx & 1;
+      mbar_wait(BAR(kBarDQFull + x), fph[x]);
+      fph[x] ^= 1;
+      tc_fence_after();
+      uint32_t v[64];
+      if (active) {
+        const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + x * 128;
+        tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      }
+      tc_fence_before();
+      mbar_arrive(BAR(kBarDQEmpty + x));
+      // staging buffer free once the previous bulk reduce has read it
+      if (warp == 4 && lane == 0) bulk_wait_read_all();
+      named_bar_sync(2, 128);
+      if (active) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sDQ + (c * D + dd) * 4), "f"(__uint_as_float(v[c])) : "memory");
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (warp == 4 && lane == 0) {
+        float* dst = p.dq_acc + (static_cast<size_t>(bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D;
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                     "r"(sDQ), "r"(Cfg::kDQBytes)
+                     : "memory");
+        bulk_commit();
+      }
+      ++idx;
+    }
+    if (warp == 4 && lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace tatn_dev
+
+// ---------------------------------------------------------------- host launcher
+namespace tatn_host {
+bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
+                     int box_rows);
+}
+
+template <int D, bool BF16>
+static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, const void* k, const void* v,
+                                     const void* o, const void* dO, const float* lse, void* dq, void* dk, void* dv,
+                                     void* ws, cudaStream_t stream, int* launches) {
+  using Cfg = tatn_dev::BwdCfg<D>;
+  const int Nq_pad = (d.Nq + 127) / 128 * 128;
+  const size_t rows = static_cast<size_t>(d.B) * d.H * Nq_pad;
+  float* dq_acc = static_cast<float*>(ws);
+  float* lse2 = dq_acc + rows * D;
+  float* delta = lse2 + rows;
+  {
+    const long long threads = static_cast<long long>(rows) * (D / 8);
+    const int blocks = static_cast<int>((threads + 255) / 256);
+    tatn_dev::tatn_bwd_pre<D, BF16><<<blocks, 256, 0, stream>>>(
+        static_cast<const uint16_t*>(o), static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
+        d.H, d.Nq, Nq_pad, lse2, delta, dq_acc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  CUtensorMap mq, mk, mv, mdo, mdk, mdv;
+  if (!tatn_host::make_map_4d_ext(&mq, d.dtype, q, D, d.Nq, d.H, d.B, d.q_str, 64) ||
+      !tatn_host::make_map_4d_ext(&mk, d.dtype, k, D, d.Nk, d.H, d.B, d.k_str, 128) ||
+      !tatn_host::make_map_4d_ext(&mv, d.dtype, v, D, d.Nk, d.H, d.B, d.v_str, 128) ||
+      !tatn_host::make_map_4d_ext(&mdo, d.dtype, dO, D, d.Nq, d.H, d.B, d.o_str, 64) ||
+      !tatn_host::make_map_4d_ext(&mdk, d.dtype, dk, D, d.Nk, d.H, d.B, d.k_str, 128) ||
+      !tatn_host::make_map_4d_ext(&mdv, d.dtype, dv, D, d.Nk, d.H, d.B, d.v_str, 128))
+    return cudaErrorInvalidValue;
+  tatn_dev::BwdParams p{};
+  p.B = d.B;
+  p.H = d.H;
+  p.Nq = d.Nq;
+  p.Nk = d.Nk;
+  p.scale_log2 = d.tau * 1.4426950408889634f;
+  p.tau = d.tau;
+  p.mask_kind = d.mask_kind;
+  p.valid_len = d.valid_len;
+  p.grid = d.block_grid;
+  p.tr = (d.Nq + 127) / 128;
+  p.tc = (d.Nk + 127) / 128;
+  p.visited = d.visited_bitmap;
+  p.lse = lse;
+  p.delta = delta;
+  p.dq_acc = dq_acc;
+  p.n_ktiles = p.tc;
+  auto kern = tatn_dev::tatn_bwd_kernel<D, BF16>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid(d.B * d.H, p.n_ktiles);
+  kern<<<grid, tatn_dev::kBwdThreads, Cfg::kSmemBytes, stream>>>(mq, mk, mv, mdo, mdk, mdv, p, lse2, Nq_pad);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  {
+    const long long threads = static_cast<long long>(d.B) * d.H * d.Nq * (D / 8);
+    const int blocks = static_cast<int>((threads + 255) / 256);
+    tatn_dev::tatn_bwd_post<D, BF16><<<blocks, 256, 0, stream>>>(dq_acc, static_cast<uint16_t*>(dq), d.q_str[0],
+                                                                 d.q_str[1], d.q_str[2], d.B, d.H, d.Nq, Nq_pad);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  *launches = 3;
+  return cudaSuccess;
+}
+
+static inline int tatn_bwd_launch(const tatn_attn_desc& d, const void* q, const void* k, const void* v, const void* o,
+                                  const void* dO, const float* lse, void* dq, void* dk, void* dv, void* ws,
+                                  cudaStream_t stream, int* launches) {
+  const bool bf16 = d.dtype == TATN_DTYPE_BF16;
+  cudaError_t e;
+  if (d.d == 128)
+    e = bf16 ? tatn_bwd_launch_t<128, true>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches)
+             : tatn_bwd_launch_t<128, false>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches);
+  else
+    e = bf16 ? tatn_bwd_launch_t<64, true>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches)
+             : tatn_bwd_launch_t<64, false>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches);
+  return e == cudaSuccess ? TATN_OK : TATN_E_CUDA;
 }

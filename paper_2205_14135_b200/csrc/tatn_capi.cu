@@ -107,6 +107,13 @@ cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
 
 }  // namespace
 
+namespace tatn_host {
+bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
+                     int box_rows) {
+  return make_map_4d(map, tma_dtype(dtype), 2, base, d, n, H, B, str, box_rows);
+}
+}  // namespace tatn_host
+
 extern "C" {
 
 int tatn_validate(const tatn_attn_desc* desc) { return validate(desc); }
@@ -170,8 +177,9 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
 
 size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc) {
   if (validate(desc) != TATN_OK) return 0;
-  const size_t rows = static_cast<size_t>(desc->B) * desc->H * desc->Nq;
-  return rows * desc->d * sizeof(float) + rows * sizeof(float) + 256;
+  // dQ accumulator [B,H,Nq_pad,d] fp32 + lse2 [B,H,Nq_pad] + D [B,H,Nq_pad], Nq_pad = roundup(Nq, 128)
+  const size_t rows = static_cast<size_t>(desc->B) * desc->H * ((desc->Nq + 127) / 128 * 128);
+  return rows * desc->d * sizeof(float) + 2 * rows * sizeof(float);
 }
 
 int tatn_bwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, const void* o, const void* dO,
