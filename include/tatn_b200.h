@@ -45,6 +45,12 @@ typedef enum {
 
 typedef enum { TATN_DTYPE_BF16 = 0, TATN_DTYPE_FP16 = 1 } tatn_dtype;
 
+/* Output precision: O (forward) and dQ/dK/dV (backward) are written either in
+ * the 16-bit input dtype or in fp32 (the "fp32 check mode" — no output
+ * rounding; the backward then also reads O as fp32). The MMAs always take the
+ * 16-bit inputs and accumulate in fp32. */
+typedef enum { TATN_OUT_INPUT_DTYPE = 0, TATN_OUT_FP32 = 1 } tatn_out_dtype;
+
 /* tatn::MaskKind (attn_config.hpp:12). Causal masks key j > query i;
  * KeyPadding masks key j >= valid_len[b] (attn_config.cpp:20-32). Custom n x n
  * masks are not on the device path (TATN_E_UNSUPPORTED). */
@@ -54,7 +60,8 @@ typedef struct {
   int32_t B, H;      /* independent (batch, head) slices                          */
   int32_t Nq, Nk;    /* query rows, key rows (Nk <= Nq: key prefix, reference.hpp:43-46) */
   int32_t d;         /* head dimension: 64 or 128                                 */
-  int32_t dtype;     /* tatn_dtype                                                */
+  int32_t dtype;     /* tatn_dtype of q, k, v, dO                                 */
+  int32_t out_dtype; /* tatn_out_dtype of o, dq, dk, dv                           */
   /* element strides of the b, h, n dimensions; d is contiguous (stride 1).
    * dO uses o_str; dQ/dK/dV use q_str/k_str/v_str. Strides must be multiples of 8. */
   int64_t q_str[3], k_str[3], v_str[3], o_str[3];
@@ -81,7 +88,8 @@ int tatn_validate(const tatn_attn_desc* desc);
 int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, void* o,
              float* lse, void* stream);
 
-/* Workspace for tatn_bwd: fp32 dQ accumulator [B,H,Nq,d] + D vector [B,H,Nq]. */
+/* Workspace for tatn_bwd: fp32 dQ accumulator [B,H,Nq_pad,d] + lse2 and D vectors
+ * [B,H,Nq_pad], Nq_pad = Nq rounded up to 128. */
 size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc);
 
 /* Backward with recomputation from lse (Algorithm 4).

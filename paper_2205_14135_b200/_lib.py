@@ -25,6 +25,9 @@ TATN_E_WORKSPACE = 6
 TATN_DTYPE_BF16 = 0
 TATN_DTYPE_FP16 = 1
 
+TATN_OUT_INPUT_DTYPE = 0
+TATN_OUT_FP32 = 1
+
 TATN_MASK_NONE = 0
 TATN_MASK_CAUSAL = 1
 TATN_MASK_KEY_PADDING = 2
@@ -51,6 +54,7 @@ class TatnAttnDesc(ctypes.Structure):
         ("Nk", ctypes.c_int32),
         ("d", ctypes.c_int32),
         ("dtype", ctypes.c_int32),
+        ("out_dtype", ctypes.c_int32),
         ("q_str", ctypes.c_int64 * 3),
         ("k_str", ctypes.c_int64 * 3),
         ("v_str", ctypes.c_int64 * 3),

@@ -50,17 +50,22 @@ class AttnSpec:
     valid_len: Optional[torch.Tensor] = None  # int32 [B] on device (key_padding)
     block_grid: Optional[torch.Tensor] = None  # uint8 [tr, tc] on device, 128x128 blocks
     visited: Optional[torch.Tensor] = None  # int32 [ceil(tr*tc/32)] on device, zeroed by caller
+    out_fp32: bool = False  # write O / dQ / dK / dV in fp32 (no output rounding)
 
 
-def make_desc(q, k, v, o, spec: AttnSpec) -> _lib.TatnAttnDesc:
+def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttnDesc:
     B, H, Nq, d = q.shape
     Nk = k.shape[2]
     desc = _lib.TatnAttnDesc()
     desc.B, desc.H, desc.Nq, desc.Nk, desc.d = B, H, Nq, Nk, d
     desc.dtype = _dtype_code(q)
-    for t in (k, v, o):
+    for t in (k, v):
         if t.dtype != q.dtype:
-            raise TypeError("q, k, v, o must share one dtype")
+            raise TypeError("q, k, v must share one dtype")
+    out_dt = torch.float32 if spec.out_fp32 else q.dtype
+    if check_o and o.dtype != out_dt:
+        raise TypeError(f"o must be {out_dt} (out_fp32={spec.out_fp32})")
+    desc.out_dtype = _lib.TATN_OUT_FP32 if spec.out_fp32 else _lib.TATN_OUT_INPUT_DTYPE
     desc.q_str[:] = _strides(q, "q")
     desc.k_str[:] = _strides(k, "k")
     desc.v_str[:] = _strides(v, "v")
@@ -95,7 +100,7 @@ def flash_fwd(q, k, v, spec: Optional[AttnSpec] = None, out=None, lse=None, stre
     lib = _lib.load()
     B, H, Nq, d = q.shape
     if out is None:
-        out = torch.empty_like(q, memory_format=torch.contiguous_format)
+        out = torch.empty(q.shape, dtype=torch.float32 if spec.out_fp32 else q.dtype, device=q.device)
     if lse is None:
         lse = torch.empty((B, H, Nq), dtype=torch.float32, device=q.device)
     desc = make_desc(q, k, v, out, spec)
@@ -109,7 +114,7 @@ def flash_fwd(q, k, v, spec: Optional[AttnSpec] = None, out=None, lse=None, stre
 def bwd_workspace(q, k, v, spec: Optional[AttnSpec] = None) -> torch.Tensor:
     spec = spec or AttnSpec()
     lib = _lib.load()
-    desc = make_desc(q, k, v, q, spec)
+    desc = make_desc(q, k, v, q, spec, check_o=False)
     n = lib.tatn_bwd_workspace_bytes(ctypes.byref(desc))
     if n == 0:
         _check(lib.tatn_validate(ctypes.byref(desc)), "tatn_bwd_workspace_bytes")
@@ -121,11 +126,20 @@ def flash_bwd(q, k, v, o, dO, lse, spec: Optional[AttnSpec] = None, dq=None, dk=
     """dQ, dK, dV = attention backward (kernels K2-K4) on device tensors."""
     spec = spec or AttnSpec()
     lib = _lib.load()
+    if dO.dtype != q.dtype:
+        raise TypeError("dO must have the input dtype")
     if dO.stride() != o.stride():
-        dO = dO.contiguous() if o.is_contiguous() else dO.as_strided(o.shape, o.stride())
-    dq = torch.empty_like(q) if dq is None else dq
-    dk = torch.empty_like(k) if dk is None else dk
-    dv = torch.empty_like(v) if dv is None else dv
+        fixed = torch.empty_strided(o.shape, o.stride(), dtype=dO.dtype, device=dO.device)
+        fixed.copy_(dO)
+        dO = fixed
+    gdt = torch.float32 if spec.out_fp32 else q.dtype
+    mk = lambda t: torch.empty_strided(t.shape, t.stride(), dtype=gdt, device=t.device)
+    dq = mk(q) if dq is None else dq
+    dk = mk(k) if dk is None else dk
+    dv = mk(v) if dv is None else dv
+    for t in (dq, dk, dv):
+        if t.dtype != gdt:
+            raise TypeError(f"gradients must be {gdt}")
     if dq.stride() != q.stride() or dk.stride() != k.stride() or dv.stride() != v.stride():
         raise ValueError("dq/dk/dv must have the strides of q/k/v")
     desc = make_desc(q, k, v, o, spec)

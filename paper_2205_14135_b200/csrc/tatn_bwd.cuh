@@ -98,8 +98,8 @@ __device__ __forceinline__ BwdSched make_bwd_sched(const BwdParams& p, int b, in
 
 // ---------------------------------------------------------------- K2
 // One 8-element chunk per thread. Rows are padded to a multiple of 128.
-template <int D, bool BF16>
-__global__ void __launch_bounds__(256) tatn_bwd_pre(const uint16_t* __restrict__ o, const uint16_t* __restrict__ dO,
+template <int D, bool BF16, bool O_F32>
+__global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_, const uint16_t* __restrict__ dO,
                                                     const float* __restrict__ lse, int64_t ob, int64_t oh, int64_t on,
                                                     int B, int H, int Nq, int Nq_pad, float* __restrict__ lse2,
                                                     float* __restrict__ delta, float* __restrict__ dq_acc) {
@@ -117,22 +117,33 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const uint16_t* __restrict__
     const int b = static_cast<int>(bh / H), h = static_cast<int>(bh % H);
     if (qi < Nq) {
       const size_t off = static_cast<size_t>(b) * ob + static_cast<size_t>(h) * oh + static_cast<size_t>(qi) * on + c * 8;
-      const uint4 ov = *reinterpret_cast<const uint4*>(o + off);
       const uint4 dv = *reinterpret_cast<const uint4*>(dO + off);
-      const uint32_t* ow = reinterpret_cast<const uint32_t*>(&ov);
       const uint32_t* dw = reinterpret_cast<const uint32_t*>(&dv);
+      float of[8];
+      if constexpr (O_F32) {
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(o_) + off);
+        const float4 a0 = src[0], a1 = src[1];
+        of[0] = a0.x; of[1] = a0.y; of[2] = a0.z; of[3] = a0.w;
+        of[4] = a1.x; of[5] = a1.y; of[6] = a1.z; of[7] = a1.w;
+      } else {
+        const uint4 ov = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(o_) + off);
+        const uint32_t* ow = reinterpret_cast<const uint32_t*>(&ov);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float2 a;
+          if constexpr (BF16) a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[k]));
+          else a = __half22float2(*reinterpret_cast<const __half2*>(&ow[k]));
+          of[2 * k] = a.x;
+          of[2 * k + 1] = a.y;
+        }
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        float2 a, bb;
-        if constexpr (BF16) {
-          a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[k]));
-          bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dw[k]));
-        } else {
-          a = __half22float2(*reinterpret_cast<const __half2*>(&ow[k]));
-          bb = __half22float2(*reinterpret_cast<const __half2*>(&dw[k]));
-        }
-        part = fmaf(a.x, bb.x, part);
-        part = fmaf(a.y, bb.y, part);
+        float2 bb;
+        if constexpr (BF16) bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dw[k]));
+        else bb = __half22float2(*reinterpret_cast<const __half2*>(&dw[k]));
+        part = fmaf(of[2 * k], bb.x, part);
+        part = fmaf(of[2 * k + 1], bb.y, part);
       }
     }
     float4* dst = reinterpret_cast<float4*>(dq_acc + row * D + c * 8);
@@ -154,8 +165,8 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const uint16_t* __restrict__
 }
 
 // ---------------------------------------------------------------- K4
-template <int D, bool BF16>
-__global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ dq_acc, uint16_t* __restrict__ dq,
+template <int D, bool BF16, bool OUT_F32>
+__global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ dq_acc, void* __restrict__ dq,
                                                      int64_t qb, int64_t qh, int64_t qn, int B, int H, int Nq,
                                                      int Nq_pad) {
   constexpr int kChunks = D / 8;
@@ -168,17 +179,23 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
   const int b = static_cast<int>(bh / H), h = static_cast<int>(bh % H);
   const float4* src = reinterpret_cast<const float4*>(dq_acc + (bh * Nq_pad + qi) * D + c * 8);
   const float4 a = src[0], bb = src[1];
-  uint4 out;
-  out.x = pack2<BF16>(a.x, a.y);
-  out.y = pack2<BF16>(a.z, a.w);
-  out.z = pack2<BF16>(bb.x, bb.y);
-  out.w = pack2<BF16>(bb.z, bb.w);
-  *reinterpret_cast<uint4*>(dq + static_cast<size_t>(b) * qb + static_cast<size_t>(h) * qh +
-                            static_cast<size_t>(qi) * qn + c * 8) = out;
+  const size_t off = static_cast<size_t>(b) * qb + static_cast<size_t>(h) * qh + static_cast<size_t>(qi) * qn + c * 8;
+  if constexpr (OUT_F32) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(dq) + off);
+    dst[0] = a;
+    dst[1] = bb;
+  } else {
+    uint4 out;
+    out.x = pack2<BF16>(a.x, a.y);
+    out.y = pack2<BF16>(a.z, a.w);
+    out.z = pack2<BF16>(bb.x, bb.y);
+    out.w = pack2<BF16>(bb.z, bb.w);
+    *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dq) + off) = out;
+  }
 }
 
 // ---------------------------------------------------------------- K3
-template <int D, bool BF16>
+template <int D, bool BF16, bool OUT_F32>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     tatn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -450,6 +467,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int which = 0; which < 2; ++which) {
       const uint32_t tacc = tmem_base + lane_off + (which == 0 ? Cfg::kTmemDK : Cfg::kTmemDV);
       const uint32_t stg = which == 0 ? sK : sV;
+      float* grow_ptr = nullptr;
+      if constexpr (OUT_F32) {
+        grow_ptr = which == 0 ? p.dk_f32 + static_cast<size_t>(b) * p.k_sb + static_cast<size_t>(h) * p.k_sh +
+                                    static_cast<size_t>(kj) * p.k_sn
+                              : p.dv_f32 + static_cast<size_t>(b) * p.v_sb + static_cast<size_t>(h) * p.v_sh +
+                                    static_cast<size_t>(kj) * p.v_sn;
+      }
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t v[32];
@@ -459,26 +483,38 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0u;
         }
-        uint32_t pk[16];
+        if constexpr (OUT_F32) {
+          if (kj < p.Nk) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pk[e] = pack2<BF16>(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-        const int sub = (c * 32) / 64;
-        const int chunk0 = ((c * 32) % 64) / 8;
-        const uint32_t rb = stg + sub * 128 * 128 + r * 128;
+            for (int e = 0; e < 8; ++e)
+              reinterpret_cast<float4*>(grow_ptr + c * 32)[e] =
+                  make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]), __uint_as_float(v[4 * e + 2]),
+                              __uint_as_float(v[4 * e + 3]));
+          }
+        } else {
+          uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          st_shared_v4(rb + (((chunk0 + e) ^ (r & 7)) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+          for (int e = 0; e < 16; ++e) pk[e] = pack2<BF16>(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+          const int sub = (c * 32) / 64;
+          const int chunk0 = ((c * 32) % 64) / 8;
+          const uint32_t rb = stg + sub * 128 * 128 + r * 128;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            st_shared_v4(rb + (((chunk0 + e) ^ (r & 7)) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        }
       }
     }
-    fence_proxy_async_smem();
-    named_bar_sync(1, 128);
-    if (r == 0) {
-      for (int s = 0; s < Cfg::kSubs; ++s) {
-        tma_store_4d(&tmDK, sK + s * 128 * 128, s * 64, sc.k0, h, b);
-        tma_store_4d(&tmDV, sV + s * 128 * 128, s * 64, sc.k0, h, b);
+    if constexpr (!OUT_F32) {
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (r == 0) {
+        for (int s = 0; s < Cfg::kSubs; ++s) {
+          tma_store_4d(&tmDK, sK + s * 128 * 128, s * 64, sc.k0, h, b);
+          tma_store_4d(&tmDV, sV + s * 128 * 128, s * 64, sc.k0, h, b);
+        }
+        bulk_commit();
+        bulk_wait_read_all();
       }
-      bulk_commit();
-      bulk_wait_read_all();
     }
   } else {
     // ------------------------------------------------------------ dQ warpgroup
@@ -541,7 +577,7 @@ bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n
                      int box_rows);
 }
 
-template <int D, bool BF16>
+template <int D, bool BF16, bool OUT_F32>
 static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, const void* k, const void* v,
                                      const void* o, const void* dO, const float* lse, void* dq, void* dk, void* dv,
                                      void* ws, cudaStream_t stream, int* launches) {
@@ -554,8 +590,8 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   {
     const long long threads = static_cast<long long>(rows) * (D / 8);
     const int blocks = static_cast<int>((threads + 255) / 256);
-    tatn_dev::tatn_bwd_pre<D, BF16><<<blocks, 256, 0, stream>>>(
-        static_cast<const uint16_t*>(o), static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
+    tatn_dev::tatn_bwd_pre<D, BF16, OUT_F32><<<blocks, 256, 0, stream>>>(
+        o, static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
         d.H, d.Nq, Nq_pad, lse2, delta, dq_acc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -565,8 +601,8 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
       !tatn_host::make_map_4d_ext(&mk, d.dtype, k, D, d.Nk, d.H, d.B, d.k_str, 128) ||
       !tatn_host::make_map_4d_ext(&mv, d.dtype, v, D, d.Nk, d.H, d.B, d.v_str, 128) ||
       !tatn_host::make_map_4d_ext(&mdo, d.dtype, dO, D, d.Nq, d.H, d.B, d.o_str, 64) ||
-      !tatn_host::make_map_4d_ext(&mdk, d.dtype, dk, D, d.Nk, d.H, d.B, d.k_str, 128) ||
-      !tatn_host::make_map_4d_ext(&mdv, d.dtype, dv, D, d.Nk, d.H, d.B, d.v_str, 128))
+      !tatn_host::make_map_4d_ext(&mdk, d.dtype, OUT_F32 ? k : dk, D, d.Nk, d.H, d.B, d.k_str, 128) ||
+      !tatn_host::make_map_4d_ext(&mdv, d.dtype, OUT_F32 ? v : dv, D, d.Nk, d.H, d.B, d.v_str, 128))
     return cudaErrorInvalidValue;
   tatn_dev::BwdParams p{};
   p.B = d.B;
@@ -585,7 +621,15 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.delta = delta;
   p.dq_acc = dq_acc;
   p.n_ktiles = p.tc;
-  auto kern = tatn_dev::tatn_bwd_kernel<D, BF16>;
+  p.dk_f32 = OUT_F32 ? static_cast<float*>(dk) : nullptr;
+  p.dv_f32 = OUT_F32 ? static_cast<float*>(dv) : nullptr;
+  p.k_sb = d.k_str[0];
+  p.k_sh = d.k_str[1];
+  p.k_sn = d.k_str[2];
+  p.v_sb = d.v_str[0];
+  p.v_sh = d.v_str[1];
+  p.v_sn = d.v_str[2];
+  auto kern = tatn_dev::tatn_bwd_kernel<D, BF16, OUT_F32>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -599,7 +643,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   {
     const long long threads = static_cast<long long>(d.B) * d.H * d.Nq * (D / 8);
     const int blocks = static_cast<int>((threads + 255) / 256);
-    tatn_dev::tatn_bwd_post<D, BF16><<<blocks, 256, 0, stream>>>(dq_acc, static_cast<uint16_t*>(dq), d.q_str[0],
+    tatn_dev::tatn_bwd_post<D, BF16, OUT_F32><<<blocks, 256, 0, stream>>>(dq_acc, dq, d.q_str[0],
                                                                  d.q_str[1], d.q_str[2], d.B, d.H, d.Nq, Nq_pad);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -611,13 +655,20 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
 static inline int tatn_bwd_launch(const tatn_attn_desc& d, const void* q, const void* k, const void* v, const void* o,
                                   const void* dO, const float* lse, void* dq, void* dk, void* dv, void* ws,
                                   cudaStream_t stream, int* launches) {
-  const bool bf16 = d.dtype == TATN_DTYPE_BF16;
-  cudaError_t e;
-  if (d.d == 128)
-    e = bf16 ? tatn_bwd_launch_t<128, true>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches)
-             : tatn_bwd_launch_t<128, false>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches);
-  else
-    e = bf16 ? tatn_bwd_launch_t<64, true>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches)
-             : tatn_bwd_launch_t<64, false>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches);
+  const int sel = (d.d == 128 ? 4 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 2 : 0) + (d.out_dtype == TATN_OUT_FP32 ? 1 : 0);
+  cudaError_t e = cudaErrorInvalidValue;
+#define TATN_BWD_CASE(i, DD, B16, F32) \
+  case i: e = tatn_bwd_launch_t<DD, B16, F32>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches); break;
+  switch (sel) {
+    TATN_BWD_CASE(0, 64, false, false)
+    TATN_BWD_CASE(1, 64, false, true)
+    TATN_BWD_CASE(2, 64, true, false)
+    TATN_BWD_CASE(3, 64, true, true)
+    TATN_BWD_CASE(4, 128, false, false)
+    TATN_BWD_CASE(5, 128, false, true)
+    TATN_BWD_CASE(6, 128, true, false)
+    TATN_BWD_CASE(7, 128, true, true)
+  }
+#undef TATN_BWD_CASE
   return e == cudaSuccess ? TATN_OK : TATN_E_CUDA;
 }

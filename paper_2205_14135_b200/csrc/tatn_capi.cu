@@ -66,6 +66,7 @@ int validate(const tatn_attn_desc* d) {
   if (d->Nk > d->Nq) return TATN_E_SHAPE;  // more keys than n (reference.cpp:25-26)
   if (d->d != 64 && d->d != 128) return TATN_E_UNSUPPORTED;
   if (d->dtype != TATN_DTYPE_BF16 && d->dtype != TATN_DTYPE_FP16) return TATN_E_UNSUPPORTED;
+  if (d->out_dtype != TATN_OUT_INPUT_DTYPE && d->out_dtype != TATN_OUT_FP32) return TATN_E_UNSUPPORTED;
   if (!(d->tau > 0.f) || !std::isfinite(d->tau)) return TATN_E_ARG;  // attn_config.cpp:52
   if (!(d->p_drop >= 0.f && d->p_drop < 1.f)) return TATN_E_ARG;      // attn_config.cpp:54
   if (d->p_drop != 0.f) return TATN_E_UNSUPPORTED;
@@ -89,11 +90,11 @@ CUtensorMapDataType tma_dtype(int dtype) {
   return dtype == TATN_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
 }
 
-template <int D, bool BF16>
+template <int D, bool BF16, bool OUT_F32>
 cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
   using Cfg = tatn_dev::FwdCfg<D>;
-  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16>;
+  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -147,7 +148,8 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   if (!make_map_4d(&mq, dt, 2, q, d.d, d.Nq, d.H, d.B, d.q_str, 128) ||
       !make_map_4d(&mk, dt, 2, k, d.d, d.Nk, d.H, d.B, d.k_str, 128) ||
       !make_map_4d(&mv, dt, 2, v, d.d, d.Nk, d.H, d.B, d.v_str, 128) ||
-      !make_map_4d(&mo, dt, 2, o, d.d, d.Nq, d.H, d.B, d.o_str, 128))
+      !make_map_4d(&mo, dt, 2, d.out_dtype == TATN_OUT_FP32 ? q : o, d.d, d.Nq, d.H, d.B,
+                   d.out_dtype == TATN_OUT_FP32 ? d.q_str : d.o_str, 128))
     return TATN_E_CUDA;
   tatn_dev::FwdParams p{};
   p.B = d.B;
@@ -165,11 +167,26 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.n_pairs = (d.Nq + 255) / 256;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
-  const bool bf16 = d.dtype == TATN_DTYPE_BF16;
-  if (d.d == 128)
-    e = bf16 ? launch_fwd<128, true>(mq, mk, mv, mo, p, s) : launch_fwd<128, false>(mq, mk, mv, mo, p, s);
-  else
-    e = bf16 ? launch_fwd<64, true>(mq, mk, mv, mo, p, s) : launch_fwd<64, false>(mq, mk, mv, mo, p, s);
+  const bool f32 = d.out_dtype == TATN_OUT_FP32;
+  p.o_f32 = f32 ? static_cast<float*>(o) : nullptr;
+  p.o_sb = d.o_str[0];
+  p.o_sh = d.o_str[1];
+  p.o_sn = d.o_str[2];
+  const int sel = (d.d == 128 ? 4 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 2 : 0) + (f32 ? 1 : 0);
+  e = cudaErrorInvalidValue;
+#define TATN_FWD_CASE(i, DD, B16, F32) \
+  case i: e = launch_fwd<DD, B16, F32>(mq, mk, mv, mo, p, s); break;
+  switch (sel) {
+    TATN_FWD_CASE(0, 64, false, false)
+    TATN_FWD_CASE(1, 64, false, true)
+    TATN_FWD_CASE(2, 64, true, false)
+    TATN_FWD_CASE(3, 64, true, true)
+    TATN_FWD_CASE(4, 128, false, false)
+    TATN_FWD_CASE(5, 128, false, true)
+    TATN_FWD_CASE(6, 128, true, false)
+    TATN_FWD_CASE(7, 128, true, true)
+  }
+#undef TATN_FWD_CASE
   if (e != cudaSuccess) return TATN_E_CUDA;
   g_last_launches = 1;
   return TATN_OK;

@@ -87,7 +87,7 @@ __device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, in
   return s;
 }
 
-template <int D, bool BF16>
+template <int D, bool BF16, bool OUT_F32>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     tatn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -334,6 +334,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(BAR(kBarOFinal + q), 0);
         tc_fence_after();
       }
+      float* orow = nullptr;
+      if constexpr (OUT_F32)
+        orow = p.o_f32 + static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
+               static_cast<size_t>(grow) * p.o_sn;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
@@ -343,29 +347,41 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = 0u;
         }
-        uint32_t pk[16];
+        if constexpr (OUT_F32) {
+          if (grow < p.Nq) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = pack2<BF16>(__uint_as_float(o[2 * i]) * inv_l, __uint_as_float(o[2 * i + 1]) * inv_l);
-        const int sub = (c * 32) / 64;
-        const int chunk0 = ((c * 32) % 64) / 8;
-        const uint32_t rbase = sO + sub * Cfg::kSubBytes + row * 128;
+            for (int i = 0; i < 8; ++i)
+              reinterpret_cast<float4*>(orow + c * 32)[i] =
+                  make_float4(__uint_as_float(o[4 * i]) * inv_l, __uint_as_float(o[4 * i + 1]) * inv_l,
+                              __uint_as_float(o[4 * i + 2]) * inv_l, __uint_as_float(o[4 * i + 3]) * inv_l);
+          }
+        } else {
+          uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t addr = rbase + (((chunk0 + j) ^ (row & 7)) << 4);
-          st_shared_v4(addr, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          for (int i = 0; i < 16; ++i)
+            pk[i] = pack2<BF16>(__uint_as_float(o[2 * i]) * inv_l, __uint_as_float(o[2 * i + 1]) * inv_l);
+          const int sub = (c * 32) / 64;
+          const int chunk0 = ((c * 32) % 64) / 8;
+          const uint32_t rbase = sO + sub * Cfg::kSubBytes + row * 128;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t addr = rbase + (((chunk0 + j) ^ (row & 7)) << 4);
+            st_shared_v4(addr, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
         }
       }
       if (grow < p.Nq) {
         const float lse = (l_run > 0.f) ? (m_run + __log2f(l_run)) * 0.69314718055994530942f : -INFINITY;
         p.lse[static_cast<size_t>(bh) * p.Nq + grow] = lse;
       }
-      fence_proxy_async_smem();
-      named_bar_sync(1 + q, 128);
-      if (row == 0) {
-        for (int s = 0; s < Cfg::kSubs; ++s) tma_store_4d(&tmO, sO + s * Cfg::kSubBytes, s * 64, sc.q0[q], h, b);
-        bulk_commit();
-        bulk_wait_read_all();
+      if constexpr (!OUT_F32) {
+        fence_proxy_async_smem();
+        named_bar_sync(1 + q, 128);
+        if (row == 0) {
+          for (int s = 0; s < Cfg::kSubs; ++s) tma_store_4d(&tmO, sO + s * Cfg::kSubBytes, s * 64, sc.q0[q], h, b);
+          bulk_commit();
+          bulk_wait_read_all();
+        }
       }
     }
   }

@@ -1,0 +1,152 @@
+"""Shared helpers for the GPU parity tests: inputs from the reference generator,
+the device call through the C ABI, and the north-star tolerance check."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import oracle as O
+from paper_2205_14135_b200 import attention as A
+
+TORCH_DT = {"bf16": torch.bfloat16, "fp16": torch.float16}
+
+# north star (BASELINE.json): 16-bit inputs, fp64 oracle on the same rounded inputs
+MAX_ABS = 2e-2
+REL_L2 = 1e-2
+
+
+def make_inputs(B, H, Nq, Nk, d, dtype):
+    q, k, v, do = O.gaussian_inputs(B, H, Nq, Nk, d)
+    return tuple(O.round_to(t, dtype) for t in (q, k, v, do))
+
+
+def to_dev(x: np.ndarray, dtype: str, layout: str = "bhnd") -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(TORCH_DT[dtype])
+    if layout == "bnhd":  # [B, N, H, d] storage viewed as [B, H, N, d] (non-contiguous strides)
+        t = t.permute(0, 2, 1, 3).contiguous().permute(0, 2, 1, 3)
+    return t.cuda()
+
+
+def empty_like_layout(t: torch.Tensor, dtype=None) -> torch.Tensor:
+    return torch.empty_strided(t.shape, t.stride(), dtype=dtype or t.dtype, device=t.device)
+
+
+def run_gpu(q, k, v, do, dtype, mask="none", valid_len=None, grid=None, backward=True, layout="bhnd",
+            visited=False, out_fp32=False):
+    """Forward (+ backward) on the device through the C ABI. Returns numpy fp64 outputs."""
+    qd, kd, vd = (to_dev(t, dtype, layout) for t in (q, k, v))
+    spec = A.AttnSpec(mask=mask, out_fp32=out_fp32)
+    if valid_len is not None:
+        spec.valid_len = torch.as_tensor(np.asarray(valid_len, dtype=np.int32)).cuda()
+    if grid is not None:
+        spec.block_grid = torch.from_numpy(np.ascontiguousarray(grid, dtype=np.uint8)).cuda()
+    Nq, Nk = q.shape[2], k.shape[2]
+    tr, tc = (Nq + 127) // 128, (Nk + 127) // 128
+    vis_f = vis_b = None
+    if visited:
+        vis_f = torch.zeros((tr * tc + 31) // 32, dtype=torch.int32, device="cuda")
+        spec.visited = vis_f
+    odt = torch.float32 if out_fp32 else None
+    o = empty_like_layout(qd, odt)
+    o, lse = A.flash_fwd(qd, kd, vd, spec, out=o)
+    assert A.last_launch_count() == 1
+    out = {"o": o.double().cpu().numpy(), "lse": lse.double().cpu().numpy()}
+    if backward:
+        if visited:
+            vis_b = torch.zeros_like(vis_f)
+            spec.visited = vis_b
+        dod = to_dev(do, dtype, layout)
+        dq, dk, dv = empty_like_layout(qd, odt), empty_like_layout(kd, odt), empty_like_layout(vd, odt)
+        A.flash_bwd(qd, kd, vd, o, dod, lse, spec, dq=dq, dk=dk, dv=dv)
+        assert A.last_launch_count() == 3
+        out.update(dq=dq.double().cpu().numpy(), dk=dk.double().cpu().numpy(), dv=dv.double().cpu().numpy())
+    torch.cuda.synchronize()
+    if visited:
+        out["visited_fwd"] = bitmap_to_grid(vis_f, tr, tc)
+        if vis_b is not None:
+            out["visited_bwd"] = bitmap_to_grid(vis_b, tr, tc)
+    return out
+
+
+def bitmap_to_grid(bm: torch.Tensor, tr: int, tc: int) -> np.ndarray:
+    words = bm.cpu().numpy().astype(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: tr * tc]
+    return bits.reshape(tr, tc).astype(np.uint8)
+
+
+def assert_close(name, got, ref, max_abs=MAX_ABS, rel_l2=REL_L2):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert got.shape == ref.shape, (name, got.shape, ref.shape)
+    if name == "lse":
+        ninf_r, ninf_g = np.isneginf(ref), np.isneginf(got)
+        assert np.array_equal(ninf_r, ninf_g), f"{name}: -inf rows differ"
+        got, ref = got[~ninf_r], ref[~ninf_r]
+        if got.size == 0:
+            return 0.0, 0.0
+    assert np.all(np.isfinite(got)), f"{name}: non-finite values"
+    err = np.abs(got - ref)
+    mx = float(err.max()) if err.size else 0.0
+    denom = float(np.linalg.norm(ref))
+    rel = float(np.linalg.norm(got - ref) / denom) if denom > 0 else float(np.linalg.norm(got - ref))
+    assert mx <= max_abs, f"{name}: max abs err {mx:.3e} > {max_abs}"
+    assert rel <= rel_l2, f"{name}: rel-L2 err {rel:.3e} > {rel_l2}"
+    return mx, rel
+
+
+def oracle_full(q, k, v, do, mask="none", valid_len=None, grid=None, backward=True):
+    o, lse = O.forward(q, k, v, mask=mask, valid_len=valid_len, grid=grid)
+    out = {"o": o, "lse": lse}
+    if backward:
+        dq, dk, dv = O.backward(q, k, v, o, do, lse, mask=mask, valid_len=valid_len, grid=grid)
+        out.update(dq=dq, dk=dk, dv=dv)
+    return out
+
+
+def make_device_inputs(B, H, N, d, dtype, keep_heads=()):
+    """Full-size inputs built slice by slice on the device (bounded host memory).
+    Returns device q, k, v, do and fp64 host copies of the slices in keep_heads."""
+    dev = {name: torch.empty((B, H, N, d), dtype=TORCH_DT[dtype], device="cuda") for name in ("q", "k", "v", "do")}
+    kept = {}
+    for b in range(B):
+        for h in range(H):
+            for which, name in enumerate(("q", "k", "v", "do")):
+                x = O.round_to(O.gaussian_matrix(N, d, O.slice_seed(b, h, H, which)), dtype)
+                dev[name][b, h] = torch.from_numpy(x.astype(np.float32)).to(TORCH_DT[dtype]).cuda()
+                if (b, h) in keep_heads:
+                    kept[(b, h, name)] = x
+    return dev, kept
+
+
+def run_device(dev, dtype, mask="none", grid=None, visited=False, out_fp32=False):
+    spec = A.AttnSpec(mask=mask, out_fp32=out_fp32)
+    N = dev["q"].shape[2]
+    tr = (N + 127) // 128
+    if grid is not None:
+        spec.block_grid = torch.from_numpy(np.ascontiguousarray(grid, dtype=np.uint8)).cuda()
+    out = {}
+    if visited:
+        spec.visited = torch.zeros((tr * tr + 31) // 32, dtype=torch.int32, device="cuda")
+    o, lse = A.flash_fwd(dev["q"], dev["k"], dev["v"], spec)
+    if visited:
+        out["visited_fwd"] = bitmap_to_grid(spec.visited, tr, tr)
+        spec.visited = torch.zeros_like(spec.visited)
+    dq, dk, dv = A.flash_bwd(dev["q"], dev["k"], dev["v"], o, dev["do"], lse, spec)
+    torch.cuda.synchronize()
+    if visited:
+        out["visited_bwd"] = bitmap_to_grid(spec.visited, tr, tr)
+    out.update(o=o, lse=lse, dq=dq, dk=dk, dv=dv)
+    return out
+
+
+def check_identities(out, dev):
+    """sum_j dK_j = 0 and sum_j dV_j = sum_i dO_i per (b, h, feature): exact for
+    softmax attention because every unmasked row of P sums to one."""
+    dk = out["dk"].double()
+    s_dk = dk.sum(dim=2)
+    scale_dk = dk.abs().sum(dim=2)
+    assert bool((s_dk.abs() <= 2e-2 * scale_dk + 0.1).all()), float((s_dk.abs() - 2e-2 * scale_dk).max())
+    s_dv = out["dv"].double().sum(dim=2)
+    s_do = dev["do"].double().sum(dim=2)
+    scale = dev["do"].double().abs().sum(dim=2)
+    assert bool(((s_dv - s_do).abs() <= 2e-2 * scale + 0.1).all()), float((s_dv - s_do).abs().max())

@@ -1,0 +1,116 @@
+"""The C-ABI library loads, exports every symbol include/tatn_b200.h declares,
+and rejects bad descriptors with the reference's error classes (CPU only: no
+compute entry point is called)."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2205_14135_b200 import _lib
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_functions():
+    text = (ROOT / "include" / "tatn_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(tatn_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_the_bound_symbols():
+    assert declared_functions() == sorted(_lib.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_exports_have_c_linkage():
+    import subprocess
+
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True,
+                         check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    for name in declared_functions():
+        assert name in exported, f"{name} is not exported unmangled"
+
+
+def test_abi_version_and_strerror():
+    lib = _lib.load()
+    assert lib.tatn_abi_version() == 1
+    for code in range(7):
+        assert _lib.strerror(code)
+    assert _lib.strerror(99) == "unknown status"
+
+
+def good_desc(**kw):
+    d = _lib.TatnAttnDesc()
+    d.B, d.H, d.Nq, d.Nk, d.d = 2, 3, 300, 300, 64
+    d.dtype = _lib.TATN_DTYPE_BF16
+    for name in ("q_str", "k_str", "v_str", "o_str"):
+        getattr(d, name)[:] = (3 * 300 * 64, 300 * 64, 64)
+    d.tau = 0.125
+    d.mask_kind = _lib.TATN_MASK_NONE
+    d.tr, d.tc = 3, 3
+    for key, val in kw.items():
+        setattr(d, key, val)
+    return d
+
+
+def validate(d):
+    return _lib.load().tatn_validate(ctypes.byref(d))
+
+
+def test_valid_descriptor_passes():
+    assert validate(good_desc()) == _lib.TATN_OK
+    assert validate(good_desc(d=128, dtype=_lib.TATN_DTYPE_FP16, mask_kind=_lib.TATN_MASK_CAUSAL)) == _lib.TATN_OK
+
+
+@pytest.mark.parametrize(
+    "kw, code",
+    [
+        (dict(B=0), _lib.TATN_E_SHAPE),
+        (dict(Nq=0), _lib.TATN_E_SHAPE),
+        (dict(Nk=301), _lib.TATN_E_SHAPE),  # more keys than n (reference.cpp:25-26)
+        (dict(d=32), _lib.TATN_E_UNSUPPORTED),
+        (dict(dtype=7), _lib.TATN_E_UNSUPPORTED),
+        (dict(tau=0.0), _lib.TATN_E_ARG),  # tau must be finite and > 0 (attn_config.cpp:52)
+        (dict(tau=float("inf")), _lib.TATN_E_ARG),
+        (dict(tau=float("nan")), _lib.TATN_E_ARG),
+        (dict(p_drop=1.0), _lib.TATN_E_ARG),  # p in [0, 1) (attn_config.cpp:54)
+        (dict(p_drop=0.1), _lib.TATN_E_UNSUPPORTED),  # dropout is not on the device path
+        (dict(mask_kind=3), _lib.TATN_E_UNSUPPORTED),  # Custom n x n masks
+        (dict(mask_kind=_lib.TATN_MASK_KEY_PADDING), _lib.TATN_E_ARG),  # no valid_len
+    ],
+)
+def test_invalid_descriptors(kw, code):
+    assert validate(good_desc(**kw)) == code
+
+
+def test_bad_strides_rejected():
+    d = good_desc()
+    d.q_str[2] = 65  # rows must be 16-byte aligned for TMA
+    assert validate(d) == _lib.TATN_E_SHAPE
+
+
+def test_block_grid_must_match_plan():
+    buf = (ctypes.c_uint8 * 9)()
+    d = good_desc(block_grid=ctypes.addressof(buf), br=128, bc=128, tr=3, tc=3)
+    assert validate(d) == _lib.TATN_OK
+    assert validate(good_desc(block_grid=ctypes.addressof(buf), br=64, bc=128, tr=3, tc=3)) == _lib.TATN_E_MASK
+    assert validate(good_desc(block_grid=ctypes.addressof(buf), br=128, bc=128, tr=2, tc=3)) == _lib.TATN_E_MASK
+
+
+def test_null_descriptor():
+    assert _lib.load().tatn_validate(None) == _lib.TATN_E_ARG
+
+
+def test_workspace_formula():
+    lib = _lib.load()
+    d = good_desc()
+    rows = 2 * 3 * 384  # Nq padded to a multiple of 128
+    assert lib.tatn_bwd_workspace_bytes(ctypes.byref(d)) == rows * 64 * 4 + 2 * rows * 4
+    assert lib.tatn_bwd_workspace_bytes(ctypes.byref(good_desc(B=0))) == 0
