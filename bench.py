@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""bench.py — attention fwd+bwd TFLOP/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload NAME] [--no-sweep] [--no-cpu-baseline]
+
+Our arm (default): one "step" is one forward (K1) + backward (K2-K4) over the
+workload's batch on each GPU, through the C ABI, with inputs resident in HBM.
+Multi-GPU (torchrun, one process per GPU): weak scaling, each rank owns its own
+(b, h) slices of the global batch (no collective on the data path); the timed
+region is bracketed by barrier + synchronize and the max over ranks is taken.
+Rank 0 prints ONE JSON line (value = whole-job TFLOP/s).
+
+--impl reference: the reference's own CPU implementation of the path
+(oracle/_ref = the reference sources compiled here; else the oracle port) on the
+host cores, same metric/config; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "attention fwd+bwd TFLOP/s (% B200 BF16 peak) vs seqlen 512-16K, d=64/128"
+UNIT = "TFLOP/s"
+
+# BASELINE.json configs. The headline (N=1) is configs[1]; the others are sweep lines.
+WORKLOADS = {
+    "gpt2-small": dict(B=8, H=12, N=1024, d=64, dtype="fp16", mask="causal",
+                       desc="GPT-2 small attention B=8 H=12 N=1024 d=64 causal fp16 (BASELINE configs[1])"),
+    "bert-large": dict(B=16, H=16, N=512, d=64, dtype="bf16", mask="key_padding",
+                       desc="BERT-large attention B=16 H=16 N=512 d=64 bf16 key padding (configs[2])"),
+    "long-2k": dict(B=8, H=32, N=2048, d=128, dtype="bf16", mask="causal", desc="configs[3] N=2K d=128 causal"),
+    "long-4k": dict(B=4, H=32, N=4096, d=128, dtype="bf16", mask="causal", desc="configs[3] N=4K d=128 causal"),
+    "long-8k": dict(B=2, H=32, N=8192, d=128, dtype="bf16", mask="causal", desc="configs[3] N=8K d=128 causal"),
+    "long-16k": dict(B=1, H=32, N=16384, d=128, dtype="bf16", mask="causal", desc="configs[3] N=16K d=128 causal"),
+    "long-4k-noncausal": dict(B=4, H=32, N=4096, d=128, dtype="bf16", mask="none",
+                              desc="configs[3] shape N=4K d=128, non-causal"),
+    "long-8k-d64": dict(B=2, H=32, N=8192, d=64, dtype="bf16", mask="none", desc="N=8K d=64 non-causal"),
+    "butterfly-16k": dict(B=4, H=16, N=16384, d=64, dtype="bf16", mask="none", grid="butterfly",
+                          desc="configs[4] block-sparse butterfly N=16K d=64"),
+    "butterfly-32k": dict(B=2, H=16, N=32768, d=64, dtype="bf16", mask="none", grid="butterfly",
+                          desc="configs[4] block-sparse butterfly N=32K d=64"),
+    "butterfly-64k": dict(B=1, H=16, N=65536, d=64, dtype="bf16", mask="none", grid="butterfly",
+                          desc="configs[4] block-sparse butterfly N=64K d=64"),
+}
+SWEEP = ["bert-large", "long-2k", "long-4k", "long-8k", "long-16k", "long-4k-noncausal", "long-8k-d64",
+         "butterfly-16k", "butterfly-64k"]
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def butterfly(tr: int):
+    """block_mask.hpp:30-33: (i, j) true iff i == j or i xor j is a power of two."""
+    import numpy as np
+
+    i = np.arange(tr)[:, None]
+    j = np.arange(tr)[None, :]
+    x = i ^ j
+    return ((x == 0) | ((x & (x - 1)) == 0)).astype(np.uint8)
+
+
+def pairs(w) -> float:
+    """Computed (query, key) pairs per slice: N^2, N(N+1)/2 causal, visited*128^2 block-sparse."""
+    N = w["N"]
+    if w.get("grid") == "butterfly":
+        return float(butterfly(N // 128).sum()) * 128 * 128
+    if w["mask"] == "causal":
+        return N * (N + 1) / 2
+    return float(N * N)
+
+
+def flops(w, slices=None):
+    s = slices if slices is not None else w["B"] * w["H"]
+    p = pairs(w)
+    return 4.0 * w["d"] * p * s, 10.0 * w["d"] * p * s  # fwd, bwd (5 GEMMs incl. recompute)
+
+
+def load_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        j = json.loads(f.read_text())
+        return dict(tflops=j["bf16_tflops"], tflops_sustained=j.get("bf16_tflops_sustained"), hbm=j["hbm_gbs"],
+                    source="measured (MEASURED_PEAKS.json)")
+    return dict(tflops=1590.0, tflops_sustained=1400.0, hbm=6650.0, source="fallback (B200_PROFILING.md)")
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for _, line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "window": "whole GPU section of the bench (warm-up, timed, e2e, sweep)"}
+
+
+# ------------------------------------------------------------------------------ our arm
+def make_inputs(w, device, seed=0):
+    import numpy as np
+    import torch
+
+    from paper_2205_14135_b200 import attention as A
+
+    dt = torch.bfloat16 if w["dtype"] == "bf16" else torch.float16
+    g = torch.Generator(device=device).manual_seed(seed)
+    shape = (w["B"], w["H"], w["N"], w["d"])
+    q, k, v, do = (torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(dt) for _ in range(4))
+    spec = A.AttnSpec(mask=w["mask"])
+    if w["mask"] == "key_padding":
+        rng = np.random.default_rng(2124 + seed)  # valid_len ~ U{N-20..N}
+        spec.valid_len = torch.as_tensor(rng.integers(w["N"] - 20, w["N"] + 1, size=w["B"]).astype(np.int32),
+                                         device=device)
+    if w.get("grid") == "butterfly":
+        spec.block_grid = torch.from_numpy(butterfly(w["N"] // 128)).to(device)
+    return q, k, v, do, spec
+
+
+class Step:
+    """Preallocated forward + backward over one batch (no allocation inside the step)."""
+
+    def __init__(self, q, k, v, do, spec):
+        import torch
+
+        from paper_2205_14135_b200 import attention as A
+
+        self.A = A
+        self.q, self.k, self.v, self.do, self.spec = q, k, v, do, spec
+        self.o = torch.empty_like(q)
+        self.lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+        self.dq, self.dk, self.dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        self.ws = A.bwd_workspace(q, k, v, spec)
+
+    def fwd(self):
+        self.A.flash_fwd(self.q, self.k, self.v, self.spec, out=self.o, lse=self.lse)
+
+    def bwd(self):
+        self.A.flash_bwd(self.q, self.k, self.v, self.o, self.do, self.lse, self.spec, self.dq, self.dk, self.dv,
+                         self.ws)
+
+    def __call__(self):
+        self.fwd()
+        self.bwd()
+
+
+def timed(fn, iters, flush, warmup=3):
+    """Sum of per-iteration CUDA-event times (L2 flushed between iterations, outside the events)."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for a, b in evs:
+        flush()
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs)
+
+
+def ncu_traffic(workload: str):
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None, None
+    j = json.loads(f.read_text())
+    ent = j.get("workloads", {}).get(workload, {}).get("bwd_K3")
+    if not ent:
+        return None, None
+    return ent.get("dram_bytes_per_launch"), ent.get("source")
+
+
+def run_ours(args, env):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_14135_b200 import _lib
+    from paper_2205_14135_b200 import iomodel
+
+    w = WORKLOADS[args.workload]
+    device = torch.device("cuda", env.local_rank)
+    torch.cuda.set_device(device)
+    _lib.load()
+    peaks = load_peaks()
+    clocks = ClockSampler(env.local_rank) if env.rank == 0 else None
+    if clocks:
+        clocks.start()
+    flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    flush = lambda: flush_buf.zero_()
+
+    q, k, v, do, spec = make_inputs(w, device, seed=env.rank)
+    step = Step(q, k, v, do, spec)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, barrier + sync on both sides, max over ranks
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if env.world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    _lib.profile_enable(True)
+    for a, b in evs:
+        flush()
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    _lib.profile_enable(False)
+    if env.world > 1:
+        dist.barrier()
+    ms_total = sum(a.elapsed_time(b) for a, b in evs)
+    k1_ms, k1_n = _lib.profile_read(0)
+    k3_ms, k3_n = _lib.profile_read(1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=device)
+    if env.world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    launches_per_step = 1 + 3  # K1 | K2 K3 K4
+    f_fwd, f_bwd = flops(w)
+    total_flops = (f_fwd + f_bwd) * env.world * args.steps
+    value = total_flops / (ms_max * 1e-3) / 1e12
+
+    # ---------------- e2e through the public API with host buffers (pinned), per step:
+    # H2D q, k, v, dO -> forward -> backward -> D2H o, lse, dq, dk, dv
+    hq, hk, hv, hdo = (t_.cpu().pin_memory() for t_ in (q, k, v, do))
+    ho, hlse = torch.empty_like(hq).pin_memory(), torch.empty(step.lse.shape, dtype=torch.float32).pin_memory()
+    hdq, hdk, hdv = (torch.empty_like(hq).pin_memory() for _ in range(3))
+
+    def e2e_step():
+        step.q.copy_(hq, non_blocking=True)
+        step.k.copy_(hk, non_blocking=True)
+        step.v.copy_(hv, non_blocking=True)
+        step.do.copy_(hdo, non_blocking=True)
+        step()
+        ho.copy_(step.o, non_blocking=True)
+        hlse.copy_(step.lse, non_blocking=True)
+        hdq.copy_(step.dq, non_blocking=True)
+        hdk.copy_(step.dk, non_blocking=True)
+        hdv.copy_(step.dv, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if env.world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+    if env.world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = total_flops / (float(te.item()) * 1e-3) / 1e12
+    elt = q.element_size()
+    n_el = q.numel()
+    h2d = 4 * n_el * elt
+    d2h = 4 * n_el * elt + step.lse.numel() * 4
+
+    out = None
+    if env.rank == 0:
+        slices = w["B"] * w["H"]
+        k3_avg = k3_ms / max(k3_n, 1)
+        k1_avg = k1_ms / max(k1_n, 1)
+        k3_tf = f_bwd / (k3_avg * 1e-3) / 1e12
+        k1_tf = f_fwd / (k1_avg * 1e-3) / 1e12
+        traffic, traffic_src = ncu_traffic(args.workload)
+        rl = {"kernel": "tatn_bwd_kernel (K3: S^T, dP^T, dV, dK, dQ^T GEMMs)", "bound": "tensor",
+              "achieved": round(k3_tf, 2), "peak": peaks["tflops"], "unit": "TFLOP/s",
+              "frac": round(k3_tf / peaks["tflops"], 4), "peak_source": peaks["source"] + ", burst bf16",
+              "algorithmic_flops_per_launch": f_bwd, "avg_launch_ms": round(k3_avg, 5), "launches": k3_n,
+              "traffic": traffic, "traffic_source": traffic_src,
+              "io_bound_bytes_theorem2": iomodel.theorem2_bound_bytes(w["N"], w["d"], 2, slices, backward=True)
+              if w.get("grid") is None else None,
+              "compulsory_bytes": iomodel.compulsory_bytes(w["N"], w["d"], 2, slices, backward=True)}
+        kernels = {"fwd_K1": {"avg_launch_ms": round(k1_avg, 5), "tflops": round(k1_tf, 2),
+                              "frac_of_peak": round(k1_tf / peaks["tflops"], 4), "launches": k1_n},
+                   "bwd_K3": {"avg_launch_ms": round(k3_avg, 5), "tflops": round(k3_tf, 2),
+                              "frac_of_peak": round(k3_tf / peaks["tflops"], 4), "launches": k3_n}}
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": env.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic N(0,1) q, k, v, dO",
+            "config": {"workload": w["desc"], "model": args.workload, "global_batch": w["B"] * env.world,
+                       "heads": w["H"], "seq_len": w["N"], "head_dim": w["d"], "mask": w["mask"],
+                       "parallelism": f"(b,h)-sharded x{env.world}, no collective",
+                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                       "flops_per_step_per_gpu": f_fwd + f_bwd,
+                       "flop_count": "fwd 4*d*P, bwd 10*d*P per slice; P = N(N+1)/2 causal, N^2 otherwise"},
+            "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "attention.flash_fwd/flash_bwd (C ABI) with pinned host buffers copied in and out"},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": rl,
+            "kernels": kernels,
+        }
+    # ---------------- sweep of the other BASELINE configs (rank 0, N=1 only)
+    if env.rank == 0 and env.world == 1 and not args.no_sweep:
+        sweep = []
+        for name in SWEEP:
+            ws = WORKLOADS[name]
+            try:
+                sq, sk, sv, sdo, sspec = make_inputs(ws, device)
+                st = Step(sq, sk, sv, sdo, sspec)
+                it = 5
+                fms = timed(st.fwd, it, flush) / it
+                st.fwd()
+                bms = timed(st.bwd, it, flush) / it
+                ff, fb = flops(ws)
+                sweep.append({"workload": name, "desc": ws["desc"], "fwd_ms": round(fms, 4), "bwd_ms": round(bms, 4),
+                              "fwd_tflops": round(ff / fms / 1e9, 1), "bwd_tflops": round(fb / bms / 1e9, 1),
+                              "fwd_bwd_tflops": round((ff + fb) / (fms + bms) / 1e9, 1),
+                              "fwd_frac": round(ff / fms / 1e9 / peaks["tflops"], 4),
+                              "bwd_frac": round(fb / bms / 1e9 / peaks["tflops"], 4)})
+                del sq, sk, sv, sdo, st
+                torch.cuda.empty_cache()
+            except Exception as e:  # report, keep the headline
+                sweep.append({"workload": name, "error": repr(e)})
+        out["sweep"] = sweep
+        out["sweep_note"] = "per-kernel-call CUDA-event times, L2 flushed between calls; frac vs measured burst peak"
+    if clocks:
+        out["clocks"] = clocks.stop()
+    if env.rank == 0 and env.world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(w)
+    return out
+
+
+# ------------------------------------------------------------------------------ CPU legs (oracle/)
+def _cpu_sample(w, steps=1):
+    """Time the reference's CPU path on a bounded sample: one (b, h) slice per host
+    thread per step. Returns (tflops, seconds, slices, threads, kind, sample text)."""
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    N, d, mask = w["N"], w["d"], w["mask"]
+    memeff = N >= 8192
+    if w.get("grid"):
+        mask = "none"  # the reference has no block-sparse engine; time its dense path on the slice shape
+    slices = threads
+    kind = "reference" if O.have_ref() else "port"
+    secs = []
+    for _ in range(steps):
+        if kind == "reference":
+            s = O.ref_time_fwd_bwd(slices, N, d, mask if mask != "key_padding" else "none", memeff, threads)
+            if s < 0:
+                raise RuntimeError("reference CPU path threw")
+        else:
+            import numpy as np
+
+            rng = np.random.default_rng(0)
+            q, k, v, do = (rng.standard_normal((1, slices, N, d)) for _ in range(4))
+            t0 = time.perf_counter()
+            o, lse = O.forward(q, k, v, mask=mask if mask != "key_padding" else "none", threads=threads)
+            O.backward(q, k, v, o, do, lse, mask=mask if mask != "key_padding" else "none", threads=threads)
+            s = time.perf_counter() - t0
+        secs.append(s)
+    ff, fb = flops(dict(w, grid=None, mask=("causal" if w["mask"] == "causal" else "none")), slices=slices)
+    tf = (ff + fb) * steps / sum(secs) / 1e12
+    what = ("memeff_forward+memeff_backward" if memeff else "standard_forward+standard_backward")
+    sample = (f"{slices} (b,h) slices of N={N} d={d} mask={mask} per step, reference {what} fp64 "
+              f"({'oracle/_ref: reference sources compiled' if kind == 'reference' else 'oracle C port'}), "
+              f"one std::thread per slice")
+    return tf, sum(secs) / steps, slices, threads, kind, sample
+
+
+def cpu_baseline(w):
+    try:
+        tf, s, slices, threads, kind, sample = _cpu_sample(w, steps=1)
+        return {"value": round(tf, 6), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                "seconds": round(s, 3)}
+    except Exception as e:
+        return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": None, "sample": f"failed: {e!r}"}
+
+
+def run_reference(args, env):
+    w = WORKLOADS[args.workload]
+    for _ in range(args.warmup):
+        _cpu_sample(w, steps=1)
+    tf, s, slices, threads, kind, sample = _cpu_sample(w, steps=args.steps)
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(tf, 6), "unit": UNIT, "n_gpus": env.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) (tatn::gaussian_matrix)",
+        "config": {"workload": w["desc"], "model": args.workload, "global_batch": w["B"], "heads": w["H"],
+                   "seq_len": w["N"], "head_dim": w["d"], "mask": w["mask"],
+                   "parallelism": f"host threads x{threads} over (b,h) slices"},
+        "cpu_baseline": {"value": round(tf, 6), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": round(tf, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gpt2-small")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    from paper_2205_14135_b200.launcher import DistEnv, init_distributed
+
+    if args.impl == "reference":
+        env = DistEnv.from_env()
+        if env.rank != 0:
+            return
+        print(json.dumps(run_reference(args, env)), flush=True)
+        return
+    env = init_distributed("nccl")
+    if env.world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={env.world}", file=sys.stderr)
+    out = run_ours(args, env)
+    if env.rank == 0:
+        print(json.dumps(out), flush=True)
+    if env.world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

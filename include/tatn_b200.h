@@ -105,6 +105,14 @@ int tatn_abi_version(void);
 /* Number of device kernels the last tatn_fwd / tatn_bwd call on this thread launched. */
 int tatn_last_launch_count(void);
 
+/* Optional measurement hook, off by default. While enabled, tatn_fwd and tatn_bwd
+ * record CUDA events on the caller's stream around their main kernel (K1 forward,
+ * K3 backward). tatn_profile_read synchronises on the recorded events and returns
+ * the summed device milliseconds and launch count for `which` (0 = K1, 1 = K3)
+ * since the previous read, then resets that counter. */
+int tatn_profile_enable(int on);
+int tatn_profile_read(int which, double* total_ms, int* launches);
+
 #ifdef __cplusplus
 }
 #endif

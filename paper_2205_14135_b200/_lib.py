@@ -41,6 +41,8 @@ EXPORTED_SYMBOLS = (
     "tatn_strerror",
     "tatn_abi_version",
     "tatn_last_launch_count",
+    "tatn_profile_enable",
+    "tatn_profile_read",
 )
 
 
@@ -109,8 +111,26 @@ def load() -> ctypes.CDLL:
     lib.tatn_abi_version.restype = ctypes.c_int
     lib.tatn_last_launch_count.argtypes = []
     lib.tatn_last_launch_count.restype = ctypes.c_int
+    lib.tatn_profile_enable.argtypes = [ctypes.c_int]
+    lib.tatn_profile_enable.restype = ctypes.c_int
+    lib.tatn_profile_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
+    lib.tatn_profile_read.restype = ctypes.c_int
     _lib = lib
     return lib
+
+
+def profile_enable(on: bool) -> None:
+    load().tatn_profile_enable(1 if on else 0)
+
+
+def profile_read(which: int):
+    """(total device ms, launches) of the main kernel (0 = forward K1, 1 = backward K3)."""
+    ms = ctypes.c_double()
+    n = ctypes.c_int()
+    st = load().tatn_profile_read(which, ctypes.byref(ms), ctypes.byref(n))
+    if st != TATN_OK:
+        raise TatnError(st, "tatn_profile_read")
+    return ms.value, n.value
 
 
 def strerror(status: int) -> str:

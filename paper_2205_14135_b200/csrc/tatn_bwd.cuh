@@ -573,6 +573,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 // ---------------------------------------------------------------- host launcher
 namespace tatn_host {
+cudaEvent_t profile_begin(int which, cudaStream_t s);
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows);
 }
@@ -637,7 +638,9 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     attr_set = true;
   }
   dim3 grid(d.B * d.H, p.n_ktiles);
+  cudaEvent_t prof_stop = tatn_host::profile_begin(1, stream);
   kern<<<grid, tatn_dev::kBwdThreads, Cfg::kSmemBytes, stream>>>(mq, mk, mv, mdo, mdk, mdv, p, lse2, Nq_pad);
+  if (prof_stop) cudaEventRecord(prof_stop, stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   {

@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "../../include/tatn_b200.h"
 #include "tatn_bwd.cuh"
@@ -20,6 +22,38 @@
 namespace {
 
 thread_local int g_last_launches = 0;
+
+// ---- optional event timing of the main kernels (tatn_profile_*)
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Profiler& prof() {
+  static Profiler p;
+  return p;
+}
+// returns the stop event to record after the kernel (nullptr when profiling is off)
+cudaEvent_t prof_begin(int which, cudaStream_t s) {
+  Profiler& P = prof();
+  std::lock_guard<std::mutex> lk(P.mu);
+  if (!P.on) return nullptr;
+  cudaEvent_t a = P.get(), b = P.get();
+  cudaEventRecord(a, s);
+  P.pending[which].emplace_back(a, b);
+  return b;
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -109,6 +143,7 @@ cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
 }  // namespace
 
 namespace tatn_host {
+cudaEvent_t profile_begin(int which, cudaStream_t s) { return prof_begin(which, s); }
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows) {
   return make_map_4d(map, tma_dtype(dtype), 2, base, d, n, H, B, str, box_rows);
@@ -122,6 +157,34 @@ int tatn_validate(const tatn_attn_desc* desc) { return validate(desc); }
 int tatn_abi_version(void) { return TATN_B200_ABI_VERSION; }
 
 int tatn_last_launch_count(void) { return g_last_launches; }
+
+int tatn_profile_enable(int on) {
+  Profiler& P = prof();
+  std::lock_guard<std::mutex> lk(P.mu);
+  P.on = on != 0;
+  return TATN_OK;
+}
+
+int tatn_profile_read(int which, double* total_ms, int* launches) {
+  if (which < 0 || which > 1 || !total_ms || !launches) return TATN_E_ARG;
+  Profiler& P = prof();
+  std::lock_guard<std::mutex> lk(P.mu);
+  double sum = 0.0;
+  int n = 0;
+  for (auto& pr : P.pending[which]) {
+    if (cudaEventSynchronize(pr.second) != cudaSuccess) return TATN_E_CUDA;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pr.first, pr.second) != cudaSuccess) return TATN_E_CUDA;
+    sum += ms;
+    ++n;
+    P.pool.push_back(pr.first);
+    P.pool.push_back(pr.second);
+  }
+  P.pending[which].clear();
+  *total_ms = sum;
+  *launches = n;
+  return TATN_OK;
+}
 
 const char* tatn_strerror(int status) {
   switch (status) {
@@ -174,6 +237,7 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.o_sn = d.o_str[2];
   const int sel = (d.d == 128 ? 4 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 2 : 0) + (f32 ? 1 : 0);
   e = cudaErrorInvalidValue;
+  cudaEvent_t prof_stop = prof_begin(0, s);
 #define TATN_FWD_CASE(i, DD, B16, F32) \
   case i: e = launch_fwd<DD, B16, F32>(mq, mk, mv, mo, p, s); break;
   switch (sel) {
@@ -187,6 +251,7 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
     TATN_FWD_CASE(7, 128, true, true)
   }
 #undef TATN_FWD_CASE
+  if (prof_stop) cudaEventRecord(prof_stop, s);
   if (e != cudaSuccess) return TATN_E_CUDA;
   g_last_launches = 1;
   return TATN_OK;
