@@ -55,7 +55,8 @@ struct BwdCfg {
   static constexpr int kOffDQ = kOffDS + 2 * kDSBytes;
   static constexpr int kOffVec = kOffDQ + kDQBytes;
   static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
-  static constexpr int kSmemBytes = kOffBar + 256 + 1024;
+  static constexpr int kOffMask = kOffBar + 256;       // block-sparse q-tile bitmask, 128 words
+  static constexpr int kSmemBytes = kOffMask + 512;   // dynamic smem is declared __align__(1024)
   static constexpr uint32_t kTmemX = 0;    // X_x = x*128: S^T [0,64) dP^T [64,128)
   static constexpr uint32_t kTmemDV = 256;
   static constexpr uint32_t kTmemDK = 256 + D;
@@ -68,12 +69,30 @@ struct BwdSched {
   int i_end;     // one past the last candidate Q tile
   const uint8_t* gcol;  // block-sparse grid column base (grid + j), stride tc; nullptr = dense
   int tc;
+  const uint32_t* mask; // block-sparse: shared-memory bitmask over 64-row Q tiles
 
-  __device__ __forceinline__ bool member(int i) const {
-    if (gcol == nullptr) return true;
-    return gcol[static_cast<size_t>(i >> 1) * tc] != 0;
+  // first visited Q tile >= i (i_end when none)
+  __device__ __forceinline__ int next(int i) const {
+    if (gcol == nullptr) return i;
+    while (i < i_end) {
+      const int w = i >> 5;
+      const uint32_t m = mask[w] >> (i & 31);
+      if (m) return i + __ffs(m) - 1;
+      i = (w + 1) << 5;
+    }
+    return i_end;
   }
 };
+
+// duplicate each of the 16 low bits: b0 b1 ... -> b0 b0 b1 b1 ...
+__device__ __forceinline__ uint32_t spread_bits16(uint32_t x) {
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x | (x << 1);
+}
 
 __device__ __forceinline__ BwdSched make_bwd_sched(const BwdParams& p, int b, int j) {
   BwdSched s;
@@ -203,8 +222,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     const BwdParams p, const float* __restrict__ lse2, int Nq_pad) {
   using Cfg = BwdCfg<D>;
   constexpr int S = Cfg::kStages;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // 128B-swizzle atoms need 1024B alignment
+  const uint32_t smem_base = smem_u32(smem_raw);
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
 
   const uint32_t sK = smem_base + Cfg::kOffK;
@@ -230,10 +250,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
-  const int bh = blockIdx.x;
+  // 1-D grid in head groups: the key tiles of `group` heads run together, so their
+  // Q / dO tiles and fp32 dQ accumulators stay L2-resident; within a group the
+  // heaviest tiles (j = 0 under a causal mask) are dispatched first.
+  int bh, j;
+  {
+    const int per_group = p.group * p.n_ktiles;
+    const int grp = static_cast<int>(blockIdx.x) / per_group;
+    const int r = static_cast<int>(blockIdx.x) - grp * per_group;
+    const int gsz = min(p.group, p.B * p.H - grp * p.group);
+    j = r / gsz;
+    bh = grp * p.group + (r - j * gsz);
+  }
   const int b = bh / p.H;
   const int h = bh - b * p.H;
-  const int j = blockIdx.y;  // key tile (j = 0 is the heaviest under a causal mask)
+  uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
 
   if (threadIdx.x == 0) {
     mbar_init(BAR(kBarKV), 1);
@@ -255,12 +286,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_relinquish();
   }
+  BwdSched sc = make_bwd_sched(p, b, j);
+  sc.mask = mask_smem;
+  if (sc.gcol != nullptr && warp == 8) {
+    // block-sparse: read grid column j once into a bitmask over 64-row Q tiles
+    for (int base = 0; base < p.tr; base += 32) {
+      const int r = base + lane;
+      const bool v = r < p.tr && sc.gcol[static_cast<size_t>(r) * p.tc] != 0;
+      const uint32_t bits = __ballot_sync(0xffffffffu, v);
+      if (lane == 0) {
+        mask_smem[(2 * base) >> 5] = spread_bits16(bits);
+        mask_smem[((2 * base) >> 5) + 1] = spread_bits16(bits >> 16);
+      }
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  const BwdSched sc = make_bwd_sched(p, b, j);
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
@@ -276,8 +319,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       int stage = 0;
       uint32_t ph = 0;
-      for (int i = sc.i_begin; i < sc.i_end; ++i) {
-        if (!sc.member(i)) continue;
+      for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
         mbar_wait(BAR(kBarQEmpty + stage), ph ^ 1);
         const uint32_t fb = BAR(kBarQFull + stage);
         mbar_expect_tx(fb, 2 * Cfg::kQTile + Cfg::kVecBytes);
@@ -310,7 +352,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t idesc_dq = make_idesc_f16(ab, 128, kBwdQT, 1, 1);  // dQ^T (A, B MN-major)
       // list the Q tiles once (the order the producer and consumers use)
       int n = 0;
-      for (int i = sc.i_begin; i < sc.i_end; ++i) n += sc.member(i) ? 1 : 0;
+      for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) ++n;
       mbar_wait(BAR(kBarKV), 0);
       tc_fence_after();
       uint32_t qph[S];
@@ -401,8 +443,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint32_t qph[S];
     for (int s = 0; s < S; ++s) qph[s] = 0;
     int idx = 0;
-    for (int i = sc.i_begin; i < sc.i_end; ++i) {
-      if (!sc.member(i)) continue;
+    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
       const int x = idx & 1;
       const int s = idx % S;
       if (p.visited != nullptr && r == 0) {
@@ -524,8 +565,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     uint32_t fph[2] = {0, 0};
     int idx = 0;
-    for (int i = sc.i_begin; i < sc.i_end; ++i) {
-      if (!sc.member(i)) continue;
+    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
       const int x = idx & 1;
       mbar_wait(BAR(kBarDQFull + x), fph[x]);
       fph[x] ^= 1;
@@ -574,6 +614,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // ---------------------------------------------------------------- host launcher
 namespace tatn_host {
 cudaEvent_t profile_begin(int which, cudaStream_t s);
+int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head);
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows);
 }
@@ -622,6 +663,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.delta = delta;
   p.dq_acc = dq_acc;
   p.n_ktiles = p.tc;
+  p.group = tatn_host::schedule_group(d.B * d.H, p.n_ktiles, static_cast<double>(d.Nq) * D * 8.0);
   p.dk_f32 = OUT_F32 ? static_cast<float*>(dk) : nullptr;
   p.dv_f32 = OUT_F32 ? static_cast<float*>(dv) : nullptr;
   p.k_sb = d.k_str[0];
@@ -637,7 +679,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(d.B * d.H, p.n_ktiles);
+  dim3 grid(static_cast<unsigned>(d.B * d.H * p.n_ktiles));
   cudaEvent_t prof_stop = tatn_host::profile_begin(1, stream);
   kern<<<grid, tatn_dev::kBwdThreads, Cfg::kSmemBytes, stream>>>(mq, mk, mv, mdo, mdk, mdv, p, lse2, Nq_pad);
   if (prof_stop) cudaEventRecord(prof_stop, stream);

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -114,9 +115,11 @@ int validate(const tatn_attn_desc* d) {
   if (d->block_grid != nullptr) {
     if (d->br != 128 || d->bc != 128) return TATN_E_MASK;  // bmask block sizes must equal the plan's
     if (d->tr != tr || d->tc != tc) return TATN_E_MASK;
+    if (tc > 2048 || 2 * tr > 4096) return TATN_E_UNSUPPORTED;  // block-sparse bitmask capacity (N <= 256K)
   }
   if (d->visited_bitmap != nullptr && (d->tr != tr || d->tc != tc)) return TATN_E_MASK;
-  if (d->Nq > (1 << 24) || static_cast<int64_t>(d->B) * d->H > (1ll << 31) - 1) return TATN_E_SHAPE;
+  if (d->Nq > (1 << 24) || static_cast<int64_t>(d->B) * d->H * ((d->Nq + 127) / 128) > (1ll << 31) - 1)
+    return TATN_E_SHAPE;
   return TATN_OK;
 }
 
@@ -135,7 +138,7 @@ cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(p.B * p.H, p.n_pairs);
+  dim3 grid(static_cast<unsigned>(p.B * p.H * p.n_pairs));
   kern<<<grid, tatn_dev::kFwdThreads, Cfg::kSmemBytes, stream>>>(q, k, v, o, p);
   return cudaGetLastError();
 }
@@ -144,6 +147,15 @@ cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
 
 namespace tatn_host {
 cudaEvent_t profile_begin(int which, cudaStream_t s) { return prof_begin(which, s); }
+// Heads per scheduling group: enough CTAs for ~2 waves on 148 SMs (so the
+// longest-first order inside a group balances the tail) while the group's
+// per-head working set stays well inside the 126 MB L2.
+int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head) {
+  int g = (2 * 148 + tiles_per_head - 1) / tiles_per_head;
+  const int l2_cap = static_cast<int>(64.0e6 / (l2_bytes_per_head > 1.0 ? l2_bytes_per_head : 1.0));
+  g = std::min(g, std::max(1, l2_cap));
+  return std::max(1, std::min(g, heads));
+}
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows) {
   return make_map_4d(map, tma_dtype(dtype), 2, base, d, n, H, B, str, box_rows);
@@ -228,6 +240,7 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.visited = d.visited_bitmap;
   p.lse = lse;
   p.n_pairs = (d.Nq + 255) / 256;
+  p.group = tatn_host::schedule_group(d.B * d.H, p.n_pairs, static_cast<double>(d.Nk) * d.d * 4.0);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   const bool f32 = d.out_dtype == TATN_OUT_FP32;

@@ -40,22 +40,37 @@ struct FwdCfg {
   static constexpr int kOffK = 2 * kTileBytes;
   static constexpr int kOffV = kOffK + kStages * kTileBytes;
   static constexpr int kOffBar = kOffV + kStages * kTileBytes;
-  static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // + alignment slack
+  static constexpr int kOffMask = kOffBar + 256;           // block-sparse row bitmasks, 2 x 64 words
+  static constexpr int kSmemBytes = kOffMask + 512 + 1024;  // + alignment slack
   static constexpr uint32_t kTmemS = 0;
   static constexpr uint32_t kTmemO = 256;
 };
+
+constexpr int kMaxSparseTiles = 2048;  // tc limit of the block-sparse path (N <= 256K)
 
 struct FwdSched {
   int q0[2];    // first global query row of each tile
   int nkv[2];   // dense mode: number of leading K/V tiles the tile visits
   int T;        // union length (tiles 0..T-1 are candidates)
   int kv_limit; // keys >= kv_limit are masked (Nk, or min(Nk, valid_len[b]))
-  const uint8_t* row[2];
+  const uint8_t* row[2];      // block-sparse grid rows in global memory (read once)
+  const uint32_t* mask[2];    // the same rows as shared-memory bitmasks
   bool sparse;
 
   __device__ __forceinline__ bool member(int q, int t) const {
-    if (sparse) return row[q] != nullptr && row[q][t] != 0;
+    if (sparse) return (mask[q][t >> 5] >> (t & 31)) & 1u;
     return t < nkv[q];
+  }
+  // first tile >= t visited by either Q tile (T when none)
+  __device__ __forceinline__ int next(int t) const {
+    if (!sparse) return t;
+    while (t < T) {
+      const int w = t >> 5;
+      const uint32_t m = (mask[0][w] | mask[1][w]) >> (t & 31);
+      if (m) return t + __ffs(m) - 1;
+      t = (w + 1) << 5;
+    }
+    return T;
   }
 };
 
@@ -116,11 +131,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
-  const int bh = blockIdx.x;
+  // 1-D grid in head groups: the CTAs of `group` heads are dispatched together
+  // (their K/V stay L2-resident), heaviest causal tiles first within the group
+  // (longest-processing-time order, so the tail is made of light tiles).
+  int bh, slot;
+  {
+    const int per_group = p.group * p.n_pairs;
+    const int grp = static_cast<int>(blockIdx.x) / per_group;
+    const int r = static_cast<int>(blockIdx.x) - grp * per_group;
+    const int gsz = min(p.group, p.B * p.H - grp * p.group);
+    slot = r / gsz;
+    bh = grp * p.group + (r - slot * gsz);
+  }
   const int b = bh / p.H;
   const int h = bh - b * p.H;
-  const int pair = (p.mask_kind == kMaskCausal && p.grid == nullptr) ? (p.n_pairs - 1 - static_cast<int>(blockIdx.y))
-                                                                     : static_cast<int>(blockIdx.y);
+  const int pair = (p.mask_kind == kMaskCausal && p.grid == nullptr) ? (p.n_pairs - 1 - slot) : slot;
+  uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
 
   if (threadIdx.x == 0) {
     mbar_init(BAR(kBarQ), 1);
@@ -142,12 +168,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_relinquish();
   }
+  FwdSched sc = make_fwd_sched(p, b, pair);
+  sc.mask[0] = mask_smem;
+  sc.mask[1] = mask_smem + kMaxSparseTiles / 32;
+  if (sc.sparse && warp == 8) {
+    // block-sparse: read the two grid rows once (coalesced) into shared-memory bitmasks
+    for (int q = 0; q < 2; ++q)
+      for (int base = 0; base < p.tc; base += 32) {
+        const int t = base + lane;
+        const bool v = sc.row[q] != nullptr && t < p.tc && sc.row[q][t] != 0;
+        const uint32_t bits = __ballot_sync(0xffffffffu, v);
+        if (lane == 0) mask_smem[q * (kMaxSparseTiles / 32) + (base >> 5)] = bits;
+      }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  const FwdSched sc = make_fwd_sched(p, b, pair);
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
@@ -162,8 +199,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tma_load_4d(sQ + q * Cfg::kTileBytes + s * Cfg::kSubBytes, &tmQ, BAR(kBarQ), s * 64, sc.q0[q], h, b);
       int stage = 0;
       uint32_t ph = 0;
-      for (int t = 0; t < sc.T; ++t) {
-        if (!sc.member(0, t) && !sc.member(1, t)) continue;
+      for (int t = sc.next(0); t < sc.T; t = sc.next(t + 1)) {
         mbar_wait(BAR(kBarKEmpty + stage), ph ^ 1);
         mbar_expect_tx(BAR(kBarKFull + stage), Cfg::kTileBytes);
         for (int s = 0; s < Cfg::kSubs; ++s)
@@ -190,37 +226,47 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc_fence_after();
       uint32_t acc[2] = {0, 0};
       uint32_t pph[2] = {0, 0};
+      const uint32_t qb[2] = {sQ, sQ + Cfg::kTileBytes};
+      auto issue_qk = [&](int q, int t, int stage) {
+        const uint32_t kbase = sK + stage * Cfg::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * Cfg::kSubBytes + (kk & 3) * 32;
+          mma_ss(tmem_base + Cfg::kTmemS + q * 128, make_sdesc_sw128(qb[q] + off, 16, 1024),
+                 make_sdesc_sw128(kbase + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(BAR(kBarSFull + q));
+        if (p.visited != nullptr) {
+          const long long bit = static_cast<long long>(pair * 2 + q) * p.tc + t;
+          atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
+        }
+      };
+      // Schedule per K/V tile t (union order over the CTA's two Q tiles):
+      //   PV_A(t), QK_A(t+1), PV_B(t), QK_B(t+1)
+      // so softmax A(t+1) starts while softmax B(t) still runs (ping-pong). The
+      // look-ahead QK goes only one tile ahead, which keeps the ring deadlock-free
+      // when the two tiles visit different block-sparse columns.
+      int t = sc.next(0);
       int stage = 0;
       uint32_t ph = 0;
-      for (int t = 0; t < sc.T; ++t) {
-        const bool mem[2] = {sc.member(0, t), sc.member(1, t)};
-        if (!mem[0] && !mem[1]) continue;
-        mbar_wait(BAR(kBarKFull + stage), ph);
+      if (t < sc.T) {
+        mbar_wait(BAR(kBarKFull + 0), 0);
         tc_fence_after();
-        const uint32_t kbase = sK + stage * Cfg::kTileBytes;
-        for (int q = 0; q < 2; ++q) {
-          if (!mem[q]) continue;
-          const uint32_t qbase = sQ + q * Cfg::kTileBytes;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * Cfg::kSubBytes + (kk & 3) * 32;
-            const uint64_t a = make_sdesc_sw128(qbase + off, 16, 1024);
-            const uint64_t bdesc = make_sdesc_sw128(kbase + off, 16, 1024);
-            mma_ss(tmem_base + Cfg::kTmemS + q * 128, a, bdesc, idesc_qk, kk > 0 ? 1u : 0u);
-          }
-          mma_commit(BAR(kBarSFull + q));
-          if (p.visited != nullptr) {
-            const int qt = pair * 2 + q;
-            const long long bit = static_cast<long long>(qt) * p.tc + t;
-            atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
-          }
-        }
-        mma_commit(BAR(kBarKEmpty + stage));
+        for (int q = 0; q < 2; ++q)
+          if (sc.member(q, t)) issue_qk(q, t, 0);
+        mma_commit(BAR(kBarKEmpty + 0));
+      }
+      while (t < sc.T) {
+        const int tn = sc.next(t + 1);
+        const int sn = (stage + 1 == Cfg::kStages) ? 0 : stage + 1;
+        const uint32_t phn = (sn == 0) ? (ph ^ 1) : ph;
+        bool k_ready = false;
+        bool qk_done[2] = {false, false};
         mbar_wait(BAR(kBarVFull + stage), ph);
         tc_fence_after();
         const uint32_t vbase = sV + stage * Cfg::kTileBytes;
         for (int q = 0; q < 2; ++q) {
-          if (!mem[q]) continue;
+          if (!sc.member(q, t)) continue;
           mbar_wait(BAR(kBarPFull + q), pph[q]);
           pph[q] ^= 1;
           tc_fence_after();
@@ -228,16 +274,36 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int kk = 0; kk < kBN / 16; ++kk) {
             // V tile is MN-major for this product: 16 keys = 2 x 1024B swizzle atoms.
             const uint64_t bdesc = make_sdesc_sw128(vbase + kk * 2048, Cfg::kSubBytes, 1024);
-            mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemS + q * 128 + kk * 8, bdesc,
-                   idesc_pv, (acc[q] | (kk > 0 ? 1u : 0u)));
+            mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemS + q * 128 + kk * 8, bdesc, idesc_pv,
+                   (acc[q] | (kk > 0 ? 1u : 0u)));
           }
           acc[q] = 1;
+          if (tn < sc.T && sc.member(q, tn)) {
+            if (!k_ready) {
+              mbar_wait(BAR(kBarKFull + sn), phn);
+              tc_fence_after();
+              k_ready = true;
+            }
+            issue_qk(q, tn, sn);
+            qk_done[q] = true;
+          }
         }
         mma_commit(BAR(kBarVEmpty + stage));
-        if (++stage == Cfg::kStages) {
-          stage = 0;
-          ph ^= 1;
+        if (tn < sc.T) {
+          for (int q = 0; q < 2; ++q) {
+            if (qk_done[q] || !sc.member(q, tn)) continue;
+            if (!k_ready) {
+              mbar_wait(BAR(kBarKFull + sn), phn);
+              tc_fence_after();
+              k_ready = true;
+            }
+            issue_qk(q, tn, sn);
+          }
+          mma_commit(BAR(kBarKEmpty + sn));
         }
+        t = tn;
+        stage = sn;
+        ph = phn;
       }
       mma_commit(BAR(kBarOFinal + 0));
       mma_commit(BAR(kBarOFinal + 1));
@@ -259,7 +325,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     int n_done = 0;
     uint32_t sph = 0;
 
-    for (int t = 0; t < sc.T; ++t) {
+    for (int t = sc.next(0); t < sc.T; t = sc.next(t + 1)) {
       if (!sc.member(q, t)) continue;
       mbar_wait(BAR(kBarSFull + q), sph);
       sph ^= 1;

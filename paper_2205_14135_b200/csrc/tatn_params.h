@@ -19,6 +19,7 @@ struct FwdParams {
   uint32_t* visited;         // optional tr*tc bitmap of tiles the kernel computed
   float* lse;                // [B, H, Nq] natural-log logsumexp (fp32)
   int n_pairs;               // ceil(Nq / 256): CTAs per (b, h)
+  int group;                 // heads per scheduling group (CTA order, see tatn_fwd_kernel)
   float* o_f32;              // fp32 output mode: O written here directly (strides below)
   int64_t o_sb, o_sh, o_sn;
 };
@@ -36,6 +37,7 @@ struct BwdParams {
   float* delta;      // [B, H, Nq] workspace: D_i = rowsum(dO_i * O_i)
   float* dq_acc;     // [B, H, Nq, d] fp32 workspace
   int n_ktiles;      // ceil(Nk / 128)
+  int group;         // heads per scheduling group (CTA order, see tatn_bwd_kernel)
   float* dk_f32;     // fp32 output mode: dK / dV written directly (strides below)
   float* dv_f32;
   int64_t k_sb, k_sh, k_sn, v_sb, v_sh, v_sn;
