@@ -12,7 +12,8 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "lib" / "libtatn_b200.so"
+# TATN_B200_LIB may point at an alternative in-tree build (tuning experiments); default is the product library
+LIB_PATH = Path(os.environ.get("TATN_B200_LIB", _PKG / "lib" / "libtatn_b200.so"))
 
 TATN_OK = 0
 TATN_E_ARG = 1
@@ -111,6 +112,9 @@ def load() -> ctypes.CDLL:
     lib.tatn_abi_version.restype = ctypes.c_int
     lib.tatn_last_launch_count.argtypes = []
     lib.tatn_last_launch_count.restype = ctypes.c_int
+    if hasattr(lib, "tatn_debug_set_trace"):  # -DTATN_TRACE builds only
+        lib.tatn_debug_set_trace.argtypes = [ctypes.c_void_p]
+        lib.tatn_debug_set_trace.restype = ctypes.c_int
     lib.tatn_profile_enable.argtypes = [ctypes.c_int]
     lib.tatn_profile_enable.restype = ctypes.c_int
     lib.tatn_profile_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]

@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // ---------------------------------------------------------------- host launcher
 namespace tatn_host {
 cudaEvent_t profile_begin(int which, cudaStream_t s);
-int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head);
+int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm);
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows);
 }
@@ -663,7 +663,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.delta = delta;
   p.dq_acc = dq_acc;
   p.n_ktiles = p.tc;
-  p.group = tatn_host::schedule_group(d.B * d.H, p.n_ktiles, static_cast<double>(d.Nq) * D * 8.0);
+  p.group = tatn_host::schedule_group(d.B * d.H, p.n_ktiles, static_cast<double>(d.Nq) * D * 8.0, 1);
   p.dk_f32 = OUT_F32 ? static_cast<float*>(dk) : nullptr;
   p.dv_f32 = OUT_F32 ? static_cast<float*>(dv) : nullptr;
   p.k_sb = d.k_str[0];

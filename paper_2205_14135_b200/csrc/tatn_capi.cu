@@ -20,6 +20,11 @@
 #include "tatn_bwd.cuh"
 #include "tatn_fwd.cuh"
 
+namespace tatn_host {
+int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm = 1);
+}
+using tatn_host::schedule_group;
+
 namespace {
 
 thread_local int g_last_launches = 0;
@@ -127,19 +132,25 @@ CUtensorMapDataType tma_dtype(int dtype) {
   return dtype == TATN_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
 }
 
-template <int D, bool BF16, bool OUT_F32>
+#ifndef TATN_FWD_NQ_D64
+#define TATN_FWD_NQ_D64 1  // d = 64: one Q tile per CTA, two CTAs per SM
+#endif
+template <int D, bool BF16, bool OUT_F32, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
 cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
-  using Cfg = tatn_dev::FwdCfg<D>;
-  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32>;
+  using Cfg = tatn_dev::FwdCfg<D, NQ>;
+  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(static_cast<unsigned>(p.B * p.H * p.n_pairs));
-  kern<<<grid, tatn_dev::kFwdThreads, Cfg::kSmemBytes, stream>>>(q, k, v, o, p);
+  tatn_dev::FwdParams pp = p;
+  pp.n_pairs = (p.Nq + 128 * NQ - 1) / (128 * NQ);  // Q-tile groups (of NQ tiles) per head
+  pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * D * 4.0, NQ == 2 ? 1 : 2);
+  dim3 grid(static_cast<unsigned>(p.B * p.H * pp.n_pairs));
+  kern<<<grid, tatn_dev::fwd_threads<NQ>(), Cfg::kSmemBytes, stream>>>(q, k, v, o, pp);
   return cudaGetLastError();
 }
 
@@ -150,8 +161,8 @@ cudaEvent_t profile_begin(int which, cudaStream_t s) { return prof_begin(which, 
 // Heads per scheduling group: enough CTAs for ~2 waves on 148 SMs (so the
 // longest-first order inside a group balances the tail) while the group's
 // per-head working set stays well inside the 126 MB L2.
-int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head) {
-  int g = (2 * 148 + tiles_per_head - 1) / tiles_per_head;
+int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm) {
+  int g = (2 * 148 * ctas_per_sm + tiles_per_head - 1) / tiles_per_head;
   const int l2_cap = static_cast<int>(64.0e6 / (l2_bytes_per_head > 1.0 ? l2_bytes_per_head : 1.0));
   g = std::min(g, std::max(1, l2_cap));
   return std::max(1, std::min(g, heads));
@@ -169,6 +180,14 @@ int tatn_validate(const tatn_attn_desc* desc) { return validate(desc); }
 int tatn_abi_version(void) { return TATN_B200_ABI_VERSION; }
 
 int tatn_last_launch_count(void) { return g_last_launches; }
+
+#ifdef TATN_TRACE
+// debug builds only: per-CTA globaltimer trace of the forward kernel (scripts/trace_fwd.py)
+int tatn_debug_set_trace(void* dev_buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  return cudaMemcpyToSymbol(tatn_dev::g_tatn_trace, &p, sizeof(p)) == cudaSuccess ? TATN_OK : TATN_E_CUDA;
+}
+#endif
 
 int tatn_profile_enable(int on) {
   Profiler& P = prof();
@@ -239,8 +258,8 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.tc = (d.Nk + 127) / 128;
   p.visited = d.visited_bitmap;
   p.lse = lse;
-  p.n_pairs = (d.Nq + 255) / 256;
-  p.group = tatn_host::schedule_group(d.B * d.H, p.n_pairs, static_cast<double>(d.Nk) * d.d * 4.0);
+  p.n_pairs = 0;  // set per variant in launch_fwd
+  p.group = 1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   const bool f32 = d.out_dtype == TATN_OUT_FP32;

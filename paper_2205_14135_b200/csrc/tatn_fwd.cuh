@@ -8,17 +8,20 @@
 // so here each CTA owns two 128-row Q tiles and streams K/V tiles through
 // shared memory: O, l, m never leave the SM until the final write.
 //
-// CTA layout (320 threads):
+// CTA layout (384 threads; setmaxnreg gives the softmax warpgroups 208 registers):
 //   warps 0-3  softmax/correction/epilogue for Q tile A (one TMEM lane per thread)
 //   warps 4-7  same for Q tile B
 //   warp  8    TMA producer (Q once, K/V ring)
 //   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 10-11 idle (complete the third warpgroup for setmaxnreg)
 // TMEM (512 cols): S_A [0,128) S_B [128,256) O_A [256,256+D) O_B [256+D, 256+2D);
 // P (bf16/fp16) overwrites the first 64 columns of S_q once S_q is in registers.
 // Per K/V tile t the MMA issues S_q = Q_q K_t^T for both tiles, then
 // O_q += P_q V_t after softmax_q signals P ready; tcgen05 ops from one thread
 // execute in order, so the next S_q write cannot overtake the P_q read.
 #pragma once
+
+#include <type_traits>
 
 #include "sm100_ptx.cuh"
 #include "tatn_params.h"
@@ -27,23 +30,39 @@ namespace tatn_dev {
 
 constexpr int kBM = 128;  // query rows per Q tile
 constexpr int kBN = 128;  // keys per K/V tile
-constexpr int kFwdThreads = 320;
+// NQ = 2: 384 threads (softmax A, softmax B, {TMA, MMA, 2 idle}), 1 CTA/SM.
+// NQ = 1: 192 threads (softmax, TMA, MMA), 2 CTAs/SM (d = 64).
+template <int NQ>
+constexpr int fwd_threads() { return NQ == 2 ? 384 : 192; }
 constexpr float kRescaleThreshold = 8.0f;  // lazy O rescale (log2 units)
+// 16-bit exponentials (ex2.approx.{bf16x2,f16x2}, one MUFU op per pair) instead of fp32
+// ex2: measured slower on B200 (r01 sweep) and less accurate, so off by default.
+#ifndef TATN_EX2_16
+#define TATN_EX2_16 0
+#endif
+// exp2 pairs per group of 8 computed by the polynomial on the FMA pipe instead of MUFU
+// (MUFU.EX2 retires 16/clk/SM). Swept on B200 (r01): 1 of 8 is best (+3-5%); 2 or 3 of 8
+// lose to the extra FMA-pipe issue. Full tiles only (masked tiles hold -inf).
+#ifndef TATN_EMU_PAIRS
+#define TATN_EMU_PAIRS 1
+#endif
+constexpr int kEmuPairs = TATN_EMU_PAIRS;
 
-template <int D>
+template <int D, int NQ = 2>
 struct FwdCfg {
   static constexpr int kSubs = D / 64;                   // 128B-swizzle column blocks
   static constexpr int kSubBytes = 128 * 128;            // 128 rows x 128 bytes
   static constexpr int kTileBytes = kSubs * kSubBytes;   // one 128 x D tile (16-bit)
-  static constexpr int kStages = (D == 128) ? 2 : 4;
+  static constexpr int kStages = (NQ == 2 && D == 64) ? 4 : 2;
   static constexpr int kOffQ = 0;
-  static constexpr int kOffK = 2 * kTileBytes;
+  static constexpr int kOffK = NQ * kTileBytes;
   static constexpr int kOffV = kOffK + kStages * kTileBytes;
   static constexpr int kOffBar = kOffV + kStages * kTileBytes;
   static constexpr int kOffMask = kOffBar + 256;           // block-sparse row bitmasks, 2 x 64 words
   static constexpr int kSmemBytes = kOffMask + 512 + 1024;  // + alignment slack
   static constexpr uint32_t kTmemS = 0;
-  static constexpr uint32_t kTmemO = 256;
+  static constexpr uint32_t kTmemO = NQ * 128;
+  static constexpr uint32_t kTmemCols = NQ == 2 ? 512 : 256;  // power of two
 };
 
 constexpr int kMaxSparseTiles = 2048;  // tc limit of the block-sparse path (N <= 256K)
@@ -74,6 +93,7 @@ struct FwdSched {
   }
 };
 
+template <int NQ>
 __device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, int pair) {
   FwdSched s;
   s.sparse = p.grid != nullptr;
@@ -84,11 +104,11 @@ __device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, in
   s.T = 0;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int qt = pair * 2 + q;
+    const int qt = pair * NQ + q;
     s.q0[q] = qt * kBM;
     s.row[q] = nullptr;
     int n = 0;
-    if (s.q0[q] < p.Nq) {
+    if (q < NQ && s.q0[q] < p.Nq) {
       if (s.sparse) {
         s.row[q] = (qt < p.tr) ? p.grid + static_cast<size_t>(qt) * p.tc : nullptr;
       } else {
@@ -102,12 +122,30 @@ __device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, in
   return s;
 }
 
-template <int D, bool BF16, bool OUT_F32>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+#ifdef TATN_TRACE
+__device__ unsigned long long* g_tatn_trace = nullptr;  // [grid][8] globaltimer stamps (debug builds only)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TATN_TRACE_AT(slot)                                                                     \
+  do {                                                                                          \
+    if (g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + (slot)] = gtimer();   \
+  } while (0)
+#else
+#define TATN_TRACE_AT(slot) \
+  do {                      \
+  } while (0)
+#endif
+
+template <int D, bool BF16, bool OUT_F32, int NQ>
+__global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     tatn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const FwdParams p) {
-  using Cfg = FwdCfg<D>;
+  using Cfg = FwdCfg<D, NQ>;
+  constexpr int kProducerWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
@@ -147,6 +185,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int h = bh - b * p.H;
   const int pair = (p.mask_kind == kMaskCausal && p.grid == nullptr) ? (p.n_pairs - 1 - slot) : slot;
   uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
+  if (threadIdx.x == 0) TATN_TRACE_AT(0);
 
   if (threadIdx.x == 0) {
     mbar_init(BAR(kBarQ), 1);
@@ -164,14 +203,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     (void)kNumBars;
     fence_mbar_init();
   }
-  if (warp == 9) {
-    tmem_alloc(smem_u32(tmem_slot), 512);
+  if (warp == kMmaWarp) {
+    tmem_alloc(smem_u32(tmem_slot), Cfg::kTmemCols);
     tmem_relinquish();
   }
-  FwdSched sc = make_fwd_sched(p, b, pair);
+  FwdSched sc = make_fwd_sched<NQ>(p, b, pair);
   sc.mask[0] = mask_smem;
   sc.mask[1] = mask_smem + kMaxSparseTiles / 32;
-  if (sc.sparse && warp == 8) {
+  if (sc.sparse && warp == kProducerWarp) {
     // block-sparse: read the two grid rows once (coalesced) into shared-memory bitmasks
     for (int q = 0; q < 2; ++q)
       for (int base = 0; base < p.tc; base += 32) {
@@ -185,135 +224,177 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 8) {
+  int n_steps_dbg = 0;
+  (void)n_steps_dbg;
+  if (warp >= kProducerWarp) {
+  if constexpr (NQ == 2) setmaxnreg_dec<80>();  // the whole third warpgroup, before it splits by role
+  if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // whole warp runs the loop (waits), one elected lane issues
+    if (elect_one_sync()) {
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmO);
-      mbar_expect_tx(BAR(kBarQ), 2 * Cfg::kTileBytes);
-      for (int q = 0; q < 2; ++q)
+      mbar_expect_tx(BAR(kBarQ), NQ * Cfg::kTileBytes);
+      for (int q = 0; q < NQ; ++q)
         for (int s = 0; s < Cfg::kSubs; ++s)
           tma_load_4d(sQ + q * Cfg::kTileBytes + s * Cfg::kSubBytes, &tmQ, BAR(kBarQ), s * 64, sc.q0[q], h, b);
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int t = sc.next(0); t < sc.T; t = sc.next(t + 1)) {
-        mbar_wait(BAR(kBarKEmpty + stage), ph ^ 1);
+    }
+    __syncwarp();
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int t = sc.next(0); t < sc.T; t = sc.next(t + 1)) {
+      mbar_wait(BAR(kBarKEmpty + stage), ph ^ 1);
+      if (elect_one_sync()) {
         mbar_expect_tx(BAR(kBarKFull + stage), Cfg::kTileBytes);
         for (int s = 0; s < Cfg::kSubs; ++s)
           tma_load_4d(sK + stage * Cfg::kTileBytes + s * Cfg::kSubBytes, &tmK, BAR(kBarKFull + stage), s * 64,
                       t * kBN, h, b);
-        mbar_wait(BAR(kBarVEmpty + stage), ph ^ 1);
+      }
+      __syncwarp();
+      mbar_wait(BAR(kBarVEmpty + stage), ph ^ 1);
+      if (elect_one_sync()) {
         mbar_expect_tx(BAR(kBarVFull + stage), Cfg::kTileBytes);
         for (int s = 0; s < Cfg::kSubs; ++s)
           tma_load_4d(sV + stage * Cfg::kTileBytes + s * Cfg::kSubBytes, &tmV, BAR(kBarVFull + stage), s * 64,
                       t * kBN, h, b);
-        if (++stage == Cfg::kStages) {
-          stage = 0;
-          ph ^= 1;
-        }
+      }
+      __syncwarp();
+      if (++stage == Cfg::kStages) {
+        stage = 0;
+        ph ^= 1;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t ab = BF16 ? 1u : 0u;
-      constexpr uint32_t idesc_qk = make_idesc_f16(ab, 128, kBN, 0, 0);
-      constexpr uint32_t idesc_pv = make_idesc_f16(ab, 128, D, 0, 1);
-      mbar_wait(BAR(kBarQ), 0);
-      tc_fence_after();
-      uint32_t acc[2] = {0, 0};
-      uint32_t pph[2] = {0, 0};
-      const uint32_t qb[2] = {sQ, sQ + Cfg::kTileBytes};
-      auto issue_qk = [&](int q, int t, int stage) {
-        const uint32_t kbase = sK + stage * Cfg::kTileBytes;
+    // whole warp runs the schedule (waits); one elected lane issues tcgen05.mma/commit.
+    constexpr uint32_t ab = BF16 ? 1u : 0u;
+    constexpr uint32_t idesc_qk = make_idesc_f16(ab, 128, kBN, 0, 0);
+    constexpr uint32_t idesc_pv = make_idesc_f16(ab, 128, D, 0, 1);
+    // base descriptors; per-MMA operands add (byte offset >> 4) to the start-address field
+    const uint64_t qdesc0 = make_sdesc_sw128(sQ, 16, 1024);
+    const uint64_t kdesc0 = make_sdesc_sw128(sK, 16, 1024);
+    const uint64_t vdesc0 = make_sdesc_sw128(sV, Cfg::kSubBytes, 1024);
+    mbar_wait(BAR(kBarQ), 0);
+    tc_fence_after();
+    TATN_TRACE_AT(7);
+    uint32_t acc[2] = {0, 0};
+    uint32_t pph[2] = {0, 0};
+    auto issue_qk = [&](int q, int t, int stage) {
+      if (elect_one_sync()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * Cfg::kSubBytes + (kk & 3) * 32;
-          mma_ss(tmem_base + Cfg::kTmemS + q * 128, make_sdesc_sw128(qb[q] + off, 16, 1024),
-                 make_sdesc_sw128(kbase + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
+          mma_ss(tmem_base + Cfg::kTmemS + q * 128, qdesc0 + ((q * Cfg::kTileBytes + off) >> 4),
+                 kdesc0 + ((stage * Cfg::kTileBytes + off) >> 4), idesc_qk, kk > 0 ? 1u : 0u);
         }
         mma_commit(BAR(kBarSFull + q));
         if (p.visited != nullptr) {
-          const long long bit = static_cast<long long>(pair * 2 + q) * p.tc + t;
+          const long long bit = static_cast<long long>(pair * NQ + q) * p.tc + t;
           atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
         }
-      };
-      // Schedule per K/V tile t (union order over the CTA's two Q tiles):
-      //   PV_A(t), QK_A(t+1), PV_B(t), QK_B(t+1)
-      // so softmax A(t+1) starts while softmax B(t) still runs (ping-pong). The
-      // look-ahead QK goes only one tile ahead, which keeps the ring deadlock-free
-      // when the two tiles visit different block-sparse columns.
-      int t = sc.next(0);
-      int stage = 0;
-      uint32_t ph = 0;
-      if (t < sc.T) {
-        mbar_wait(BAR(kBarKFull + 0), 0);
-        tc_fence_after();
-        for (int q = 0; q < 2; ++q)
-          if (sc.member(q, t)) issue_qk(q, t, 0);
-        mma_commit(BAR(kBarKEmpty + 0));
       }
-      while (t < sc.T) {
-        const int tn = sc.next(t + 1);
-        const int sn = (stage + 1 == Cfg::kStages) ? 0 : stage + 1;
-        const uint32_t phn = (sn == 0) ? (ph ^ 1) : ph;
-        bool k_ready = false;
-        bool qk_done[2] = {false, false};
-        mbar_wait(BAR(kBarVFull + stage), ph);
+      __syncwarp();
+    };
+    // Schedule per K/V tile t (union order over the CTA's two Q tiles):
+    //   PV_A(t), QK_A(t+1), PV_B(t), QK_B(t+1)
+    // so softmax A(t+1) starts while softmax B(t) still runs (ping-pong). The
+    // look-ahead QK goes only one tile ahead, which keeps the ring deadlock-free
+    // when the two tiles visit different block-sparse columns.
+    int t = sc.next(0);
+    int stage = 0;
+    uint32_t ph = 0;
+#ifdef TATN_TRACE
+    int dbg_pv = 0;
+#endif
+    if (t < sc.T) {
+      mbar_wait(BAR(kBarKFull + 0), 0);
+      tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (sc.member(q, t)) issue_qk(q, t, 0);
+      if (elect_one_sync()) mma_commit(BAR(kBarKEmpty + 0));
+      __syncwarp();
+    }
+    while (t < sc.T) {
+      const int tn = sc.next(t + 1);
+      const int sn = (stage + 1 == Cfg::kStages) ? 0 : stage + 1;
+      const uint32_t phn = (sn == 0) ? (ph ^ 1) : ph;
+      bool k_ready = false;
+      bool qk_done[2] = {false, false};
+      mbar_wait(BAR(kBarVFull + stage), ph);
+      tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (!sc.member(q, t)) continue;
+        mbar_wait(BAR(kBarPFull + q), pph[q]);
+        pph[q] ^= 1;
         tc_fence_after();
-        const uint32_t vbase = sV + stage * Cfg::kTileBytes;
-        for (int q = 0; q < 2; ++q) {
-          if (!sc.member(q, t)) continue;
-          mbar_wait(BAR(kBarPFull + q), pph[q]);
-          pph[q] ^= 1;
-          tc_fence_after();
+#ifdef TATN_TRACE
+        if (q == 0 && ++dbg_pv == 3) TATN_TRACE_AT(11);
+#endif
+        if (elect_one_sync()) {
 #pragma unroll
           for (int kk = 0; kk < kBN / 16; ++kk) {
             // V tile is MN-major for this product: 16 keys = 2 x 1024B swizzle atoms.
-            const uint64_t bdesc = make_sdesc_sw128(vbase + kk * 2048, Cfg::kSubBytes, 1024);
-            mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemS + q * 128 + kk * 8, bdesc, idesc_pv,
-                   (acc[q] | (kk > 0 ? 1u : 0u)));
-          }
-          acc[q] = 1;
-          if (tn < sc.T && sc.member(q, tn)) {
-            if (!k_ready) {
-              mbar_wait(BAR(kBarKFull + sn), phn);
-              tc_fence_after();
-              k_ready = true;
-            }
-            issue_qk(q, tn, sn);
-            qk_done[q] = true;
+            mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemS + q * 128 + kk * 8,
+                   vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv, (acc[q] | (kk > 0 ? 1u : 0u)));
           }
         }
-        mma_commit(BAR(kBarVEmpty + stage));
-        if (tn < sc.T) {
-          for (int q = 0; q < 2; ++q) {
-            if (qk_done[q] || !sc.member(q, tn)) continue;
-            if (!k_ready) {
-              mbar_wait(BAR(kBarKFull + sn), phn);
-              tc_fence_after();
-              k_ready = true;
-            }
-            issue_qk(q, tn, sn);
+        __syncwarp();
+        acc[q] = 1;
+        if (tn < sc.T && sc.member(q, tn)) {
+          if (!k_ready) {
+            mbar_wait(BAR(kBarKFull + sn), phn);
+            tc_fence_after();
+            k_ready = true;
           }
-          mma_commit(BAR(kBarKEmpty + sn));
+          issue_qk(q, tn, sn);
+          qk_done[q] = true;
+#ifdef TATN_TRACE
+          if (q == 0 && dbg_pv == 3) TATN_TRACE_AT(12);
+#endif
         }
-        t = tn;
-        stage = sn;
-        ph = phn;
       }
-      mma_commit(BAR(kBarOFinal + 0));
-      mma_commit(BAR(kBarOFinal + 1));
+      if (elect_one_sync()) mma_commit(BAR(kBarVEmpty + stage));
+      __syncwarp();
+      if (tn < sc.T) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          if (qk_done[q] || !sc.member(q, tn)) continue;
+          if (!k_ready) {
+            mbar_wait(BAR(kBarKFull + sn), phn);
+            tc_fence_after();
+            k_ready = true;
+          }
+          issue_qk(q, tn, sn);
+        }
+        if (elect_one_sync()) mma_commit(BAR(kBarKEmpty + sn));
+        __syncwarp();
+      }
+      t = tn;
+      stage = sn;
+      ph = phn;
     }
+    if (elect_one_sync())
+      for (int q = 0; q < NQ; ++q) mma_commit(BAR(kBarOFinal + q));
+    __syncwarp();
+  }
   } else {
+    if constexpr (NQ == 2) setmaxnreg_inc<208>();  // 2*128*(208-168) <= 128*(168-80)
     // ------------------------------------------------------------ softmax warpgroups
     const int q = warp >> 2;               // Q tile of this warpgroup
+    // this warpgroup's schedule as scalars (no dynamically indexed struct -> no local memory)
+    const int my_q0 = (q == 0) ? sc.q0[0] : sc.q0[1];
+    const int my_nkv = (q == 0) ? sc.nkv[0] : sc.nkv[1];
+    const uint32_t* my_mask = (q == 0) ? sc.mask[0] : sc.mask[1];
+    auto is_member = [&](int t) -> bool {
+      return sc.sparse ? (((my_mask[t >> 5] >> (t & 31)) & 1u) != 0u) : (t < my_nkv);
+    };
     const int wq = warp & 3;               // TMEM lane quadrant
     const int row = wq * 32 + lane;        // row within the tile == TMEM lane
-    const int grow = sc.q0[q] + row;       // global query row
+    const int grow = my_q0 + row;       // global query row
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t tS = tmem_base + lane_off + Cfg::kTmemS + q * 128;
     const uint32_t tO = tmem_base + lane_off + Cfg::kTmemO + q * D;
@@ -326,34 +407,48 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     uint32_t sph = 0;
 
     for (int t = sc.next(0); t < sc.T; t = sc.next(t + 1)) {
-      if (!sc.member(q, t)) continue;
+      if (!is_member(t)) continue;
       mbar_wait(BAR(kBarSFull + q), sph);
+      if (threadIdx.x == 0 && n_done == 0) TATN_TRACE_AT(1);
+      if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(8);
+      if (threadIdx.x == 0 && n_done == 3) TATN_TRACE_AT(13);
       sph ^= 1;
       tc_fence_after();
-      uint32_t sr[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-
       const int k0 = t * kBN;
-      const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > sc.q0[q]);
-      if (need_mask) {
+      const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0);
+      // masked scores -> -inf (diagonal / boundary tiles only)
+      auto apply_mask = [&](uint32_t (&r)[32], int c) {
+        if (need_mask) {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          const int kj = k0 + i;
-          const bool masked = (kj >= sc.kv_limit) || (causal && kj > grow);
-          if (masked) sr[i] = __float_as_uint(-INFINITY);
+          for (int i = 0; i < 32; ++i) {
+            const int kj = k0 + c * 32 + i;
+            if ((kj >= sc.kv_limit) || (causal && kj > grow)) r[i] = __float_as_uint(-INFINITY);
+          }
+        }
+      };
+      // pass 1: row max, streaming S from TMEM in 32-column chunks (3-input max);
+      // the load of chunk c+1 is in flight while chunk c is reduced
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+      {
+        uint32_t ra[32], rb[32];
+        tmem_ld32_async(tS, ra);
+        tmem_ld_wait32(ra);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t (&cur)[32] = (c & 1) ? rb : ra;
+          uint32_t (&nxt)[32] = (c & 1) ? ra : rb;
+          if (c + 1 < 4) tmem_ld32_async(tS + (c + 1) * 32, nxt);
+          apply_mask(cur, c);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            mx0 = fmax3(mx0, __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]));
+            mx1 = fmax3(mx1, __uint_as_float(cur[i + 2]), __uint_as_float(cur[i + 3]));
+          }
+          if (c + 1 < 4) tmem_ld_wait32(nxt);
         }
       }
-      float mx0 = __uint_as_float(sr[0]), mx1 = __uint_as_float(sr[1]);
-      float mx2 = __uint_as_float(sr[2]), mx3 = __uint_as_float(sr[3]);
-#pragma unroll
-      for (int i = 4; i < 128; i += 4) {
-        mx0 = fmaxf(mx0, __uint_as_float(sr[i]));
-        mx1 = fmaxf(mx1, __uint_as_float(sr[i + 1]));
-        mx2 = fmaxf(mx2, __uint_as_float(sr[i + 2]));
-        mx3 = fmaxf(mx3, __uint_as_float(sr[i + 3]));
-      }
-      const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const float m_tile = fmaxf(mx0, mx1) * sl2;
+      if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(9);
       float alpha = 1.f;
       if (m_tile - m_run > kRescaleThreshold) {  // false for NaN (both -inf)
         alpha = ex2_approx(m_run - m_tile);      // 0 when m_run == -inf
@@ -372,27 +467,71 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float rs0 = 0.f, rs1 = 0.f;
-      uint32_t pk[64];
+      // pass 2: p = 2^(s*scale_log2 - m) per 32-column chunk (FFMA2 scale, MUFU ex2 or
+      // the FMA-pipe polynomial for (i & 7) < kEmuPairs on full tiles); P (16-bit)
+      // is stored over S columns [16c, 16c+16), which pass 2 has already consumed.
+      const uint64_t sl2x2 = f2_pack(sl2, sl2), negm = f2_pack(-m_use, -m_use);
+      uint64_t rsum0 = f2_pack(0.f, 0.f), rsum1 = rsum0;
+      uint32_t ra[32], rb[32];
+      tmem_ld32_async(tS, ra);
+      tmem_ld_wait32(ra);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float p0 = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), sl2, -m_use));
-        const float p1 = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), sl2, -m_use));
-        rs0 += p0;
-        rs1 += p1;
-        pk[i] = pack2<BF16>(p0, p1);
+      for (int c = 0; c < 4; ++c) {
+        uint32_t (&r)[32] = (c & 1) ? rb : ra;
+        uint32_t (&nxt)[32] = (c & 1) ? ra : rb;
+        if (c + 1 < 4) tmem_ld32_async(tS + (c + 1) * 32, nxt);
+        apply_mask(r, c);
+        uint32_t pk[16];
+        // straight-line bodies: the polynomial pairs interleave with the MUFU pairs
+        auto exp_chunk = [&](auto emu_on) {
+          constexpr bool kEmu = decltype(emu_on)::value;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int i = c * 16 + k;
+            const uint64_t x =
+                f2_fma(f2_pack(__uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1])), sl2x2, negm);
+            uint64_t pv;
+            if constexpr (TATN_EX2_16 && !OUT_F32) {
+              float x0, x1;
+              f2_unpack(x, x0, x1);
+              pk[k] = ex2_pair16<BF16>(x0, x1);
+              pv = widen_pair16<BF16>(pk[k]);  // l sums exactly the P the MMA consumes
+            } else {
+              if (kEmu && (i & 7) < kEmuPairs) {
+                pv = exp2_poly_f2(x);
+              } else {
+                float x0, x1;
+                f2_unpack(x, x0, x1);
+                pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
+              }
+              float p0, p1;
+              f2_unpack(pv, p0, p1);
+              pk[k] = pack2<BF16>(p0, p1);
+            }
+            if (k & 1) rsum1 = f2_add(rsum1, pv);
+            else rsum0 = f2_add(rsum0, pv);
+          }
+        };
+        if (kEmuPairs > 0 && !need_mask) exp_chunk(std::true_type{});
+        else exp_chunk(std::false_type{});
+        tmem_st16(tS + c * 16, pk);
+        if (c + 1 < 4) tmem_ld_wait32(nxt);
       }
-      l_run += rs0 + rs1;
-      tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      float rs0, rs1, rs2, rs3;
+      f2_unpack(rsum0, rs0, rs1);
+      f2_unpack(rsum1, rs2, rs3);
+      l_run += (rs0 + rs1) + (rs2 + rs3);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(BAR(kBarPFull + q));
+      if (threadIdx.x == 0) TATN_TRACE_AT(2);
+      if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(10);
       ++n_done;
     }
 
+    n_steps_dbg = n_done;
     // ------------------------------------------------------------ epilogue
-    if (sc.q0[q] < p.Nq) {
+    if (my_q0 < p.Nq) {
       mbar_wait(BAR(kBarQ), 0);  // Q_q smem is reused as the O staging buffer
       const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
       const uint32_t sO = sQ + q * Cfg::kTileBytes;
@@ -400,6 +539,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(BAR(kBarOFinal + q), 0);
         tc_fence_after();
       }
+      if (threadIdx.x == 0) TATN_TRACE_AT(3);
       float* orow = nullptr;
       if constexpr (OUT_F32)
         orow = p.o_f32 + static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
@@ -444,7 +584,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         fence_proxy_async_smem();
         named_bar_sync(1 + q, 128);
         if (row == 0) {
-          for (int s = 0; s < Cfg::kSubs; ++s) tma_store_4d(&tmO, sO + s * Cfg::kSubBytes, s * 64, sc.q0[q], h, b);
+          for (int s = 0; s < Cfg::kSubs; ++s) tma_store_4d(&tmO, sO + s * Cfg::kSubBytes, s * 64, my_q0, h, b);
           bulk_commit();
           bulk_wait_read_all();
         }
@@ -454,10 +594,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (threadIdx.x == 0) {
+    TATN_TRACE_AT(4);
+#ifdef TATN_TRACE
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    if (g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 5] = smid;
+    if (g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 6] = static_cast<unsigned long long>(n_steps_dbg);
+#endif
+  }
+  if (warp == kMmaWarp) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
 }
 
