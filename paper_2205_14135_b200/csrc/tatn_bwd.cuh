@@ -307,7 +307,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // whole warp runs the loop (waits), one elected lane issues
+    if (elect_one_sync()) {
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
@@ -317,10 +318,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_4d(sK + s * 128 * 128, &tmK, BAR(kBarKV), s * 64, sc.k0, h, b);
         tma_load_4d(sV + s * 128 * 128, &tmV, BAR(kBarKV), s * 64, sc.k0, h, b);
       }
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
-        mbar_wait(BAR(kBarQEmpty + stage), ph ^ 1);
+    }
+    __syncwarp();
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
+      mbar_wait(BAR(kBarQEmpty + stage), ph ^ 1);
+      if (elect_one_sync()) {
         const uint32_t fb = BAR(kBarQFull + stage);
         mbar_expect_tx(fb, 2 * Cfg::kQTile + Cfg::kVecBytes);
         for (int s = 0; s < Cfg::kSubs; ++s) {
@@ -337,99 +341,112 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                          vdst + kBwdQT * 4),
                      "l"(srcd), "r"(kBwdQT * 4), "r"(fb)
                      : "memory");
-        if (++stage == S) {
-          stage = 0;
-          ph ^= 1;
-        }
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        ph ^= 1;
       }
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t ab = BF16 ? 1u : 0u;
-      constexpr uint32_t idesc_s = make_idesc_f16(ab, 128, kBwdQT, 0, 0);   // S^T, dP^T
-      constexpr uint32_t idesc_acc = make_idesc_f16(ab, 128, D, 0, 1);      // dV, dK (B MN-major)
-      constexpr uint32_t idesc_dq = make_idesc_f16(ab, 128, kBwdQT, 1, 1);  // dQ^T (A, B MN-major)
-      // list the Q tiles once (the order the producer and consumers use)
-      int n = 0;
-      for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) ++n;
-      mbar_wait(BAR(kBarKV), 0);
-      tc_fence_after();
-      uint32_t qph[S];
-      for (int s = 0; s < S; ++s) qph[s] = 0;
-      uint32_t pph[2] = {0, 0}, eph[2] = {0, 0};
+    // whole warp runs the schedule (waits); one elected lane issues tcgen05.mma/commit
+    constexpr uint32_t ab = BF16 ? 1u : 0u;
+    constexpr uint32_t idesc_s = make_idesc_f16(ab, 128, kBwdQT, 0, 0);   // S^T, dP^T
+    constexpr uint32_t idesc_acc = make_idesc_f16(ab, 128, D, 0, 1);      // dV, dK (B MN-major)
+    constexpr uint32_t idesc_dq = make_idesc_f16(ab, 128, kBwdQT, 1, 1);  // dQ^T (A, B MN-major)
+    // base descriptors; per-MMA operands add (byte offset >> 4) to the start-address field
+    const uint64_t dK0 = make_sdesc_sw128(sK, 16, 1024);                 // K as K-major A
+    const uint64_t dV0 = make_sdesc_sw128(sV, 16, 1024);                 // V as K-major A
+    const uint64_t dQk0 = make_sdesc_sw128(sQ, 16, 1024);                // Q as K-major B
+    const uint64_t dDOk0 = make_sdesc_sw128(sDO, 16, 1024);              // dO as K-major B
+    const uint64_t dQmn0 = make_sdesc_sw128(sQ, Cfg::kQSub, 1024);       // Q as MN-major B
+    const uint64_t dDOmn0 = make_sdesc_sw128(sDO, Cfg::kQSub, 1024);     // dO as MN-major B
+    const uint64_t dKmn0 = make_sdesc_sw128(sK, 128 * 128, 1024);        // K^T as MN-major A
+    const uint64_t dDS0 = make_sdesc_sw128(sDS, 128 * 128, 1024);        // dS^T as MN-major B
+    // list the Q tiles once (the order the producer and consumers use)
+    int n = 0;
+    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) ++n;
+    mbar_wait(BAR(kBarKV), 0);
+    tc_fence_after();
+    uint32_t qph = 0;  // phase bit per Q/dO stage (bit s)
+    uint32_t pph[2] = {0, 0}, eph[2] = {0, 0};
 
-      auto front_dp = [&](int idx) {
-        const int s = idx % S;
-        const int x = idx & 1;
-        mbar_wait(BAR(kBarQFull + s), qph[s]);
-        qph[s] ^= 1;
-        tc_fence_after();
-        const uint32_t dob = sDO + s * Cfg::kQTile;
+    auto front_dp = [&](int idx) {
+      const int s = idx % S;
+      const int x = idx & 1;
+      mbar_wait(BAR(kBarQFull + s), (qph >> s) & 1u);
+      qph ^= 1u << s;
+      tc_fence_after();
+      if (elect_one_sync()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t offa = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
           const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
-          mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, make_sdesc_sw128(sV + offa, 16, 1024),
-                 make_sdesc_sw128(dob + offb, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, dV0 + (offa >> 4),
+                 dDOk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
         }
-      };
-      auto front_s = [&](int idx) {
-        const int s = idx % S;
-        const int x = idx & 1;
-        const uint32_t qb = sQ + s * Cfg::kQTile;
+      }
+      __syncwarp();
+    };
+    auto front_s = [&](int idx) {
+      const int s = idx % S;
+      const int x = idx & 1;
+      if (elect_one_sync()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t offa = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
           const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
-          mma_ss(tmem_base + Cfg::kTmemX + x * 128, make_sdesc_sw128(sK + offa, 16, 1024),
-                 make_sdesc_sw128(qb + offb, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128, dK0 + (offa >> 4), dQk0 + ((s * Cfg::kQTile + offb) >> 4),
+                 idesc_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(BAR(kBarSFull + x));
-      };
-
-      for (int idx = 0; idx < n && idx < 2; ++idx) {
-        front_dp(idx);
-        front_s(idx);
       }
-      for (int idx = 0; idx < n; ++idx) {
-        const int x = idx & 1;
-        const int s = idx % S;
-        mbar_wait(BAR(kBarPFull + x), pph[x]);
-        pph[x] ^= 1;
-        tc_fence_after();
-        const uint32_t qb = sQ + s * Cfg::kQTile;
-        const uint32_t dob = sDO + s * Cfg::kQTile;
-        const uint32_t accf = idx > 0 ? 1u : 0u;
+      __syncwarp();
+    };
+
+    for (int idx = 0; idx < n && idx < 2; ++idx) {
+      front_dp(idx);
+      front_s(idx);
+    }
+    for (int idx = 0; idx < n; ++idx) {
+      const int x = idx & 1;
+      const int s = idx % S;
+      mbar_wait(BAR(kBarPFull + x), pph[x]);
+      pph[x] ^= 1;
+      tc_fence_after();
+      const uint32_t accf = idx > 0 ? 1u : 0u;
+      if (elect_one_sync()) {
         // dV += P^T dO   (P^T bf16 in X_x cols [0,32); dO MN-major, 16 queries per step)
 #pragma unroll
         for (int kk = 0; kk < kBwdQT / 16; ++kk)
           mma_ts(tmem_base + Cfg::kTmemDV, tmem_base + Cfg::kTmemX + x * 128 + kk * 8,
-                 make_sdesc_sw128(dob + kk * 2048, Cfg::kQSub, 1024), idesc_acc, accf | (kk > 0 ? 1u : 0u));
+                 dDOmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc, accf | (kk > 0 ? 1u : 0u));
         // dK += dS^T Q   (dS^T bf16 in X_x cols [64,96))
 #pragma unroll
         for (int kk = 0; kk < kBwdQT / 16; ++kk)
           mma_ts(tmem_base + Cfg::kTmemDK, tmem_base + Cfg::kTmemX + x * 128 + 64 + kk * 8,
-                 make_sdesc_sw128(qb + kk * 2048, Cfg::kQSub, 1024), idesc_acc, accf | (kk > 0 ? 1u : 0u));
+                 dQmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc, accf | (kk > 0 ? 1u : 0u));
         // dQ^T = K^T dS^T  (K MN-major as A; dS^T MN-major as B; 16 keys per step) -> X_x cols [0,64)
-        const uint32_t dsb = sDS + (idx & 1) * Cfg::kDSBytes;
 #pragma unroll
         for (int kk = 0; kk < kBwdKT / 16; ++kk)
-          mma_ss(tmem_base + Cfg::kTmemX + x * 128, make_sdesc_sw128(sK + kk * 2048, 128 * 128, 1024),
-                 make_sdesc_sw128(dsb + kk * 2048, 128 * 128, 1024), idesc_dq, kk > 0 ? 1u : 0u);
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128, dKmn0 + ((kk * 2048) >> 4),
+                 dDS0 + (((idx & 1) * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq, kk > 0 ? 1u : 0u);
         mma_commit(BAR(kBarDQFull + x));
         mma_commit(BAR(kBarQEmpty + s));
         mma_commit(BAR(kBarDSEmpty + (idx & 1)));
-        if (idx + 2 < n) {
-          front_dp(idx + 2);  // dP^T region free: its dS^T was consumed above (in-order)
-          mbar_wait(BAR(kBarDQEmpty + x), eph[x]);  // dQ^T of this tile read out of X_x
-          eph[x] ^= 1;
-          tc_fence_after();
-          front_s(idx + 2);
-        }
       }
-      mma_commit(BAR(kBarFinal));
+      __syncwarp();
+      if (idx + 2 < n) {
+        front_dp(idx + 2);  // dP^T region free: its dS^T was consumed above (in-order)
+        mbar_wait(BAR(kBarDQEmpty + x), eph[x]);  // dQ^T of this tile read out of X_x
+        eph[x] ^= 1;
+        tc_fence_after();
+        front_s(idx + 2);
+      }
     }
+    if (elect_one_sync()) mma_commit(BAR(kBarFinal));
+    __syncwarp();
   } else if (warp < 4) {
     // ------------------------------------------------------------ softmax warpgroup
     const int r = warp * 32 + lane;  // key row within tile == TMEM lane
@@ -440,8 +457,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const bool causal = p.mask_kind == kMaskCausal;
     uint32_t sph[2] = {0, 0};
     uint32_t dsph[2] = {0, 0};
-    uint32_t qph[S];
-    for (int s = 0; s < S; ++s) qph[s] = 0;
+    uint32_t qph = 0;  // phase bit per Q/dO stage (bit s)
     int idx = 0;
     for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
       const int x = idx & 1;
@@ -450,8 +466,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const long long bit = static_cast<long long>(i >> 1) * p.tc + j;
         atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
       }
-      mbar_wait(BAR(kBarQFull + s), qph[s]);  // lse2 / D vectors landed
-      qph[s] ^= 1;
+      mbar_wait(BAR(kBarQFull + s), (qph >> s) & 1u);  // lse2 / D vectors landed
+      qph ^= 1u << s;
       mbar_wait(BAR(kBarSFull + x), sph[x]);
       sph[x] ^= 1;
       tc_fence_after();
