@@ -268,7 +268,8 @@ def run_ours(args, env):
     ms_total = sum(a.elapsed_time(b) for a, b in evs)
     k1_ms, k1_n = _lib.profile_read(0)
     k3_ms, k3_n = _lib.profile_read(1)
-    t = torch.tensor([ms_total], dtype=torch.float64, device=device)
+    coll_dev = device if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([ms_total], dtype=torch.float64, device=coll_dev)
     if env.world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -332,7 +333,7 @@ def run_ours(args, env):
     s_out.wait_stream(s_cmp)
     e1.record(s_out)
     torch.cuda.synchronize()
-    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=coll_dev)
     if env.world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = total_flops / (float(te.item()) * 1e-3) / 1e12

@@ -42,15 +42,22 @@ class DistEnv:
 
 
 def init_distributed(backend: str = "nccl") -> DistEnv:
-    """Initialise torch.distributed when launched by torchrun (no-op for 1 rank)."""
+    """Initialise torch.distributed when launched by torchrun (no-op for 1 rank).
+
+    TATN_DIST_BACKEND=gloo and TATN_SHARED_GPU=1 are test hooks: they let several
+    ranks share one device (gloo for the bench's timing collectives) so the
+    multi-rank path can be exercised on a single-GPU machine."""
     env = DistEnv.from_env()
+    backend = os.environ.get("TATN_DIST_BACKEND", backend)
+    if os.environ.get("TATN_SHARED_GPU") == "1":
+        env.local_rank = 0
     if env.world > 1:
         import torch.distributed as dist
 
         if not dist.is_initialized():
-            if backend == "nccl":
-                import torch
+            import torch
 
+            if backend == "nccl":
                 torch.cuda.set_device(env.local_rank)
                 dist.init_process_group("nccl", device_id=torch.device("cuda", env.local_rank))
             else:
