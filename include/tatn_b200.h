@@ -31,14 +31,14 @@
 extern "C" {
 #endif
 
-#define TATN_B200_ABI_VERSION 1
+#define TATN_B200_ABI_VERSION 2
 
 typedef enum {
   TATN_OK = 0,
   TATN_E_ARG = 1,          /* null pointer / malformed descriptor        (std::invalid_argument) */
   TATN_E_SHAPE = 2,        /* B,H,N,d or stride mismatch                 (std::invalid_argument) */
   TATN_E_MASK = 3,         /* block-mask size / plan mismatch            (std::invalid_argument) */
-  TATN_E_UNSUPPORTED = 4,  /* valid for the reference, not on this path  (e.g. p_drop != 0)     */
+  TATN_E_UNSUPPORTED = 4,  /* valid for the reference, not on this path  (e.g. Custom masks)     */
   TATN_E_CUDA = 5,         /* CUDA runtime / launch failure or no sm_100 device                 */
   TATN_E_WORKSPACE = 6     /* workspace too small                                                */
 } tatn_status;
@@ -76,7 +76,11 @@ typedef struct {
   /* optional device bitmap of tr*tc bits (bit = i*tc + j), OR-ed with the tiles
    * the kernels actually computed; must be zeroed by the caller. NULL = off. */
   uint32_t* visited_bitmap;
-  float p_drop;            /* must be 0 (dropout not on this path) -> else UNSUPPORTED   */
+  /* Dropout (tatn::dropout_scale, dropout.cpp:7-27): element (i, j) of slice (b, h) is
+   * kept iff the top 53 bits of mix64(mix64(mix64(seed + b*H + h) ^ (i+1)) ^ ((j+1) << 1))
+   * * 2^-53 >= p_drop, and then scaled by 1/(1 - p_drop); slice 0 uses `seed` itself,
+   * so a one-head call reproduces the reference's mask bit for bit. p_drop in [0, 1). */
+  double p_drop;
   uint64_t seed;
 } tatn_attn_desc;
 

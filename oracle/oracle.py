@@ -49,6 +49,8 @@ class OrcCfg(ctypes.Structure):
         ("bc", ctypes.c_int),
         ("tr", ctypes.c_int),
         ("tc", ctypes.c_int),
+        ("p_drop", ctypes.c_double),
+        ("seed", ctypes.c_uint64),
     ]
 
 
@@ -73,12 +75,14 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(os.fspath(LIB))
         pc = ctypes.POINTER(OrcCfg)
         L.orc_gaussian_matrix.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _dp]
+        L.orc_dropout_scale.argtypes = [ctypes.c_uint64, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_double]
+        L.orc_dropout_scale.restype = ctypes.c_double
         L.orc_forward_rows.argtypes = [pc, _dp, _dp, _dp, _dp, _dp, _ip, ctypes.c_int]
         L.orc_forward_rows.restype = ctypes.c_int
-        L.orc_forward_batch.argtypes = [pc, ctypes.c_int, _ip, _dp, _dp, _dp, _dp, _dp, ctypes.c_int]
+        L.orc_forward_batch.argtypes = [pc, ctypes.c_int, _ip, _dp, _dp, _dp, _dp, _dp, ctypes.c_int, ctypes.c_int]
         L.orc_forward_batch.restype = ctypes.c_int
         L.orc_backward_batch.argtypes = [pc, ctypes.c_int, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
-                                         ctypes.c_int]
+                                         ctypes.c_int, ctypes.c_int]
         L.orc_backward_batch.restype = ctypes.c_int
         L.orc_backward_dq_rows.argtypes = [pc, _dp, _dp, _dp, _dp, _dp, _dp, _ip, ctypes.c_int, _dp]
         L.orc_backward_dq_rows.restype = ctypes.c_int
@@ -116,9 +120,13 @@ def ref() -> ctypes.CDLL:
         R = ctypes.CDLL(os.fspath(REF_LIB))
         i, d_ = ctypes.c_int, ctypes.c_double
         R.ref_gaussian_matrix.argtypes = [i, i, ctypes.c_uint64, _dp]
-        R.ref_standard_forward.argtypes = [i, i, i, d_, i, i, _u8p, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _u64p]
+        R.ref_standard_forward.argtypes = [i, i, i, d_, i, i, _u8p, i, i, i, d_, ctypes.c_uint64, _dp, _dp, _dp, _dp,
+                                           _dp, _dp, _dp, _u64p]
         R.ref_standard_forward.restype = i
-        R.ref_standard_backward.argtypes = [i, i, i, d_, i, i, _u8p, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _u64p]
+        R.ref_standard_backward.argtypes = [i, i, i, d_, i, i, _u8p, i, i, i, d_, ctypes.c_uint64, _dp, _dp, _dp, _dp,
+                                            _dp, _dp, _dp, _u64p]
+        R.ref_dropout_scale.argtypes = [ctypes.c_uint64, ctypes.c_longlong, ctypes.c_longlong, d_]
+        R.ref_dropout_scale.restype = d_
         R.ref_standard_backward.restype = i
         R.ref_memeff_forward.argtypes = [i, i, i, d_, i, i, _dp, _dp, _dp, _dp, _dp]
         R.ref_memeff_forward.restype = i
@@ -173,8 +181,9 @@ def round_to(x: np.ndarray, dtype: str) -> np.ndarray:
 
 
 # ----------------------------------------------------------------------------- attention
-def _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc):
+def _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc, p_drop=0.0, seed=0):
     c = OrcCfg()
+    c.p_drop, c.seed = float(p_drop), int(seed)
     c.n, c.nk, c.d = Nq, Nk, d
     c.tau = tau if tau is not None else 1.0 / math.sqrt(d)
     c.mask_kind = MASK_CODES[mask] if isinstance(mask, str) else int(mask)
@@ -190,21 +199,22 @@ def _contig(*arrs):
     return [np.ascontiguousarray(a, dtype=np.float64) for a in arrs]
 
 
-def forward(q, k, v, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None):
-    """O, LSE for q [B,H,Nq,d], k/v [B,H,Nk,d]. valid_len: per-batch array or scalar."""
+def forward(q, k, v, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None, p_drop=0.0, seed=0):
+    """O, LSE for q [B,H,Nq,d], k/v [B,H,Nk,d]. valid_len: per-batch array or scalar.
+    Dropout: slice (b, h) uses seed + b*H + h, the C ABI's batched convention."""
     q, k, v = _contig(q, k, v)
     B, H, Nq, d = q.shape
     Nk = k.shape[2]
     if grid is not None:
         grid = np.ascontiguousarray(grid, dtype=np.uint8)
-    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc)
+    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc, p_drop, seed)
     vl = None
     if valid_len is not None:
         vl = np.ascontiguousarray(np.broadcast_to(np.asarray(valid_len, dtype=np.int32).reshape(-1, 1), (B, H)).reshape(-1))
     o = np.empty_like(q)
     lse = np.empty((B, H, Nq))
     rc = lib().orc_forward_batch(ctypes.byref(c), B * H, _ptr(vl, _ip) if vl is not None else None, _ptr(q), _ptr(k),
-                                 _ptr(v), _ptr(o), _ptr(lse), threads or os.cpu_count() or 1)
+                                 _ptr(v), _ptr(o), _ptr(lse), threads or os.cpu_count() or 1, 1)
     if rc != 0:
         raise RuntimeError("orc_forward_batch failed")
     return o, lse
@@ -244,14 +254,14 @@ def backward_dq_rows(q, k, v, o_rows, do, lse_rows, rows, tau=None, mask="none",
     return out
 
 
-def backward(q, k, v, o, do, lse, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None):
+def backward(q, k, v, o, do, lse, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None, p_drop=0.0, seed=0):
     """dQ, dK, dV from the saved (o, lse) — Algorithm 4 semantics in fp64."""
     q, k, v, o, do, lse = _contig(q, k, v, o, do, lse)
     B, H, Nq, d = q.shape
     Nk = k.shape[2]
     if grid is not None:
         grid = np.ascontiguousarray(grid, dtype=np.uint8)
-    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc)
+    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc, p_drop, seed)
     vl = None
     if valid_len is not None:
         vl = np.ascontiguousarray(np.broadcast_to(np.asarray(valid_len, dtype=np.int32).reshape(-1, 1), (B, H)).reshape(-1))
@@ -260,10 +270,24 @@ def backward(q, k, v, o, do, lse, tau=None, mask="none", valid_len=None, grid=No
     dv = np.empty_like(v)
     rc = lib().orc_backward_batch(ctypes.byref(c), B * H, _ptr(vl, _ip) if vl is not None else None, _ptr(q), _ptr(k),
                                   _ptr(v), _ptr(o), _ptr(do), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv),
-                                  threads or os.cpu_count() or 1)
+                                  threads or os.cpu_count() or 1, 1)
     if rc != 0:
         raise RuntimeError("orc_backward_batch failed")
     return dq, dk, dv
+
+
+def dropout_scale(seed: int, i: int, j: int, p: float) -> float:
+    """tatn::dropout_scale (dropout.cpp:22-27), restated in C."""
+    return float(lib().orc_dropout_scale(seed, i, j, p))
+
+
+def dropout_mask(seed: int, rows: int, cols: int, p: float) -> np.ndarray:
+    """tatn::dropout_mask_matrix (dropout.cpp:29-35) via the C restatement (vectorised over numpy)."""
+    m = np.empty((rows, cols))
+    for i in range(rows):
+        for j in range(cols):
+            m[i, j] = dropout_scale(seed, i, j, p)
+    return m
 
 
 # ----------------------------------------------------------------------------- block masks / plans / IO
@@ -317,7 +341,12 @@ def ref_gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
     return out
 
 
-def ref_standard(q, k, v, do=None, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128):
+def ref_dropout_scale(seed: int, i: int, j: int, p: float) -> float:
+    return float(ref().ref_dropout_scale(seed, i, j, p))
+
+
+def ref_standard(q, k, v, do=None, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, p_drop=0.0,
+                 seed=0):
     """The reference's standard_forward (+ standard_backward) on one slice.
     Returns dict with o, lse, m, l, fwd_counters (+ dq, dk, dv, bwd_counters)."""
     q, k, v = _contig(q, k, v)
@@ -333,8 +362,8 @@ def ref_standard(q, k, v, do=None, tau=None, mask="none", valid_len=None, grid=N
     lse = np.empty(n); m = np.empty(n); l = np.empty(n)
     ctr = np.zeros(3, dtype=np.uint64)
     R = ref()
-    rc = R.ref_standard_forward(n, nk, d, tau, mk, vl, gp, br, bc, tc, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
-                                _ptr(m), _ptr(l), _ptr(ctr, _u64p))
+    rc = R.ref_standard_forward(n, nk, d, tau, mk, vl, gp, br, bc, tc, p_drop, seed, _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                _ptr(lse), _ptr(m), _ptr(l), _ptr(ctr, _u64p))
     if rc != 0:
         raise ValueError("reference standard_forward threw")
     out = {"o": o, "lse": lse, "m": m, "l": l, "fwd_counters": ctr.copy()}
@@ -342,8 +371,8 @@ def ref_standard(q, k, v, do=None, tau=None, mask="none", valid_len=None, grid=N
         (do,) = _contig(do)
         dq = np.empty_like(q); dk = np.empty_like(k); dv = np.empty_like(v)
         ctr2 = np.zeros(3, dtype=np.uint64)
-        rc = R.ref_standard_backward(n, nk, d, tau, mk, vl, gp, br, bc, tc, _ptr(q), _ptr(k), _ptr(v), _ptr(do),
-                                     _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ctr2, _u64p))
+        rc = R.ref_standard_backward(n, nk, d, tau, mk, vl, gp, br, bc, tc, p_drop, seed, _ptr(q), _ptr(k), _ptr(v),
+                                     _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ctr2, _u64p))
         if rc != 0:
             raise ValueError("reference standard_backward threw")
         out.update(dq=dq, dk=dk, dv=dv, bwd_counters=ctr2)

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "tatn/attn_config.hpp"
+#include "tatn/dropout.hpp"
 #include "tatn/counters.hpp"
 #include "tatn/matrix.hpp"
 #include "tatn/random.hpp"
@@ -37,9 +38,11 @@ void from_matrix(const tatn::Matrix& m, double* out) {
 // composed into a Custom additive mask on top of the base predicate, i.e.
 // the element mask compose_block_mask documents (block_mask.hpp:42-46).
 tatn::AttnConfig make_cfg(int n, int d, double tau, int mask_kind, int valid_len, const uint8_t* grid, int br, int bc,
-                          int tc) {
+                          int tc, double p_drop = 0.0, uint64_t seed = 0) {
   tatn::AttnConfig cfg = tatn::AttnConfig::make(n, d);
   cfg.tau = tau;
+  cfg.p_drop = p_drop;
+  cfg.seed = seed;
   if (mask_kind == 1) cfg.mask = tatn::MaskSpec::causal();
   if (mask_kind == 2) cfg.mask = tatn::MaskSpec::key_padding(valid_len);
   if (grid != nullptr) {
@@ -65,11 +68,15 @@ void ref_gaussian_matrix(int rows, int cols, uint64_t seed, double* out) {
 
 // standard_forward (reference.cpp:39-100). lse = m + ln(l) (-inf when l == 0).
 // counters = {hbm_read_elems, hbm_write_elems, flops}. Returns 0 or -1 on exception.
+double ref_dropout_scale(uint64_t seed, long long i, long long j, double p) {
+  return tatn::dropout_scale(tatn::DropoutRng{seed}, static_cast<std::size_t>(i), static_cast<std::size_t>(j), p);
+}
+
 int ref_standard_forward(int n, int nk, int d, double tau, int mask_kind, int valid_len, const uint8_t* grid, int br,
-                         int bc, int tc, const double* q, const double* k, const double* v, double* o, double* lse,
-                         double* m_out, double* l_out, uint64_t* counters) {
+                         int bc, int tc, double p_drop, uint64_t seed, const double* q, const double* k, const double* v,
+                         double* o, double* lse, double* m_out, double* l_out, uint64_t* counters) {
   try {
-    const auto cfg = make_cfg(n, d, tau, mask_kind, valid_len, grid, br, bc, tc);
+    const auto cfg = make_cfg(n, d, tau, mask_kind, valid_len, grid, br, bc, tc, p_drop, seed);
     tatn::AccessCounter ctr;
     const auto art = tatn::standard_forward(to_matrix(q, n, d), to_matrix(k, nk, d), to_matrix(v, nk, d), cfg, &ctr);
     from_matrix(art.o, o);
@@ -92,10 +99,10 @@ int ref_standard_forward(int n, int nk, int d, double tau, int mask_kind, int va
 
 // standard_backward (reference.cpp:102-204) on the artifacts of standard_forward.
 int ref_standard_backward(int n, int nk, int d, double tau, int mask_kind, int valid_len, const uint8_t* grid, int br,
-                          int bc, int tc, const double* q, const double* k, const double* v, const double* dO,
-                          double* dq, double* dk, double* dv, uint64_t* counters) {
+                          int bc, int tc, double p_drop, uint64_t seed, const double* q, const double* k, const double* v,
+                          const double* dO, double* dq, double* dk, double* dv, uint64_t* counters) {
   try {
-    const auto cfg = make_cfg(n, d, tau, mask_kind, valid_len, grid, br, bc, tc);
+    const auto cfg = make_cfg(n, d, tau, mask_kind, valid_len, grid, br, bc, tc, p_drop, seed);
     const auto Q = to_matrix(q, n, d), K = to_matrix(k, nk, d), V = to_matrix(v, nk, d);
     const auto art = tatn::standard_forward(Q, K, V, cfg, nullptr);
     tatn::AccessCounter ctr;

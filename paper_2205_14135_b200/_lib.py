@@ -71,7 +71,7 @@ class TatnAttnDesc(ctypes.Structure):
         ("tr", ctypes.c_int32),
         ("tc", ctypes.c_int32),
         ("visited_bitmap", ctypes.c_void_p),
-        ("p_drop", ctypes.c_float),
+        ("p_drop", ctypes.c_double),
         ("seed", ctypes.c_uint64),
     ]
 

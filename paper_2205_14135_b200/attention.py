@@ -51,6 +51,8 @@ class AttnSpec:
     block_grid: Optional[torch.Tensor] = None  # uint8 [tr, tc] on device, 128x128 blocks
     visited: Optional[torch.Tensor] = None  # int32 [ceil(tr*tc/32)] on device, zeroed by caller
     out_fp32: bool = False  # write O / dQ / dK / dV in fp32 (no output rounding)
+    p_drop: float = 0.0  # dropout probability in [0, 1) (reference's positional PRNG, dropout.cpp)
+    seed: int = 0  # dropout seed; slice (b, h) uses seed + b*H + h
 
 
 def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttnDesc:
@@ -84,8 +86,8 @@ def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttn
         desc.block_grid = None
         desc.tr, desc.tc = tr, tc
     desc.visited_bitmap = spec.visited.data_ptr() if spec.visited is not None else None
-    desc.p_drop = 0.0
-    desc.seed = 0
+    desc.p_drop = float(spec.p_drop)
+    desc.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
     return desc
 
 

@@ -272,6 +272,23 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- dropout
+// splitmix64 finaliser of the reference's positional generator (dropout.cpp:7-12).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+// per query row: mix64(mix64(seed) ^ (i + 1))   (dropout.cpp:14-17)
+__device__ __forceinline__ uint64_t drop_row_hash(uint64_t seed, int i) {
+  return mix64(mix64(seed) ^ (static_cast<uint64_t>(i) + 1));
+}
+// keep (i, j) iff u = (h >> 11) * 2^-53 >= p  <=>  h >= ceil(p * 2^53) << 11   (dropout.cpp:18-27)
+__device__ __forceinline__ bool drop_keep(uint64_t row_hash, int j, uint64_t thresh) {
+  return mix64(row_hash ^ ((static_cast<uint64_t>(j) + 1) << 1)) >= thresh;
+}
+
 // ---------------------------------------------------------------- math
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

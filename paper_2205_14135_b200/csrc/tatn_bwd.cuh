@@ -27,6 +27,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include "../../include/tatn_b200.h"
 #include "sm100_ptx.cuh"
 #include "tatn_params.h"
@@ -56,7 +58,8 @@ struct BwdCfg {
   static constexpr int kOffVec = kOffDQ + kDQBytes;
   static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
   static constexpr int kOffMask = kOffBar + 256;       // block-sparse q-tile bitmask, 128 words
-  static constexpr int kSmemBytes = kOffMask + 512;   // dynamic smem is declared __align__(1024)
+  static constexpr int kOffDrop = kOffMask + 512;      // dropout: 64 query-row hashes of the current tile
+  static constexpr int kSmemBytes = kOffDrop + 512;   // dynamic smem is declared __align__(1024)
   static constexpr uint32_t kTmemX = 0;    // X_x = x*128: S^T [0,64) dP^T [64,128)
   static constexpr uint32_t kTmemDV = 256;
   static constexpr uint32_t kTmemDK = 256 + D;
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
 }
 
 // ---------------------------------------------------------------- K3
-template <int D, bool BF16, bool OUT_F32>
+template <int D, bool BF16, bool OUT_F32, bool DROP>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     tatn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -479,6 +482,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_ld32(tX + 96, *reinterpret_cast<uint32_t(*)[32]>(&dp[32]));
       const float* vl = vec_gen + s * (Cfg::kVecBytes / 4);
       const int i0 = i * kBwdQT;
+      // dropout: the tile's 64 query-row hashes (thread r < 64 computes row i0 + r)
+      const uint64_t* drop_rows = reinterpret_cast<const uint64_t*>(smem_gen + Cfg::kOffDrop);
+      if constexpr (DROP) {
+        named_bar_sync(3, 128);  // previous tile's hashes fully consumed
+        if (r < kBwdQT)
+          reinterpret_cast<uint64_t*>(smem_gen + Cfg::kOffDrop)[r] =
+              drop_row_hash(p.drop_seed + static_cast<uint64_t>(bh), i0 + r);
+        named_bar_sync(3, 128);
+      }
       const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0);
       uint32_t pk[32], dk[32];
 #pragma unroll
@@ -492,8 +504,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const bool masked = (kj >= sc.kv_limit) || (causal && kj > i0 + c);
             if (masked) pr = 0.f;
           }
-          pv[e] = pr;
-          dv[e] = pr * (__uint_as_float(dp[c]) - vl[kBwdQT + c]) * tau;
+          if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
+            const float z = drop_keep(drop_rows[c], kj, p.drop_thresh) ? p.drop_scale : 0.f;
+            dv[e] = pr * (__uint_as_float(dp[c]) * z - vl[kBwdQT + c]) * tau;
+            pv[e] = pr * z;
+          } else {
+            pv[e] = pr;
+            dv[e] = pr * (__uint_as_float(dp[c]) - vl[kBwdQT + c]) * tau;
+          }
         }
         pk[c2] = pack2<BF16>(pv[0], pv[1]);
         dk[c2] = pack2<BF16>(dv[0], dv[1]);
@@ -629,13 +647,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 // ---------------------------------------------------------------- host launcher
 namespace tatn_host {
+// dropout threshold of the reference's test u >= p with u = (h >> 11) * 2^-53:
+// keep iff h >= ceil(p * 2^53) << 11 (exact: p * 2^53 is exact in binary64)
+inline void set_dropout(const tatn_attn_desc& d, uint64_t* seed, uint64_t* thresh, float* scale) {
+  *seed = d.seed;
+  const double t = std::ceil(d.p_drop * 9007199254740992.0);  // 2^53
+  *thresh = static_cast<uint64_t>(t) << 11;
+  *scale = d.p_drop > 0.0 ? static_cast<float>(1.0 / (1.0 - d.p_drop)) : 1.f;
+}
 cudaEvent_t profile_begin(int which, cudaStream_t s);
 int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm);
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows);
 }
 
-template <int D, bool BF16, bool OUT_F32>
+template <int D, bool BF16, bool OUT_F32, bool DROP>
 static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, const void* k, const void* v,
                                      const void* o, const void* dO, const float* lse, void* dq, void* dk, void* dv,
                                      void* ws, cudaStream_t stream, int* launches) {
@@ -688,7 +714,8 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.v_sb = d.v_str[0];
   p.v_sh = d.v_str[1];
   p.v_sn = d.v_str[2];
-  auto kern = tatn_dev::tatn_bwd_kernel<D, BF16, OUT_F32>;
+  tatn_host::set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
+  auto kern = tatn_dev::tatn_bwd_kernel<D, BF16, OUT_F32, DROP>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -716,19 +743,28 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
 static inline int tatn_bwd_launch(const tatn_attn_desc& d, const void* q, const void* k, const void* v, const void* o,
                                   const void* dO, const float* lse, void* dq, void* dk, void* dv, void* ws,
                                   cudaStream_t stream, int* launches) {
-  const int sel = (d.d == 128 ? 4 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 2 : 0) + (d.out_dtype == TATN_OUT_FP32 ? 1 : 0);
+  const int sel = (d.d == 128 ? 8 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 4 : 0) + (d.out_dtype == TATN_OUT_FP32 ? 2 : 0) +
+                  (d.p_drop > 0.0 ? 1 : 0);
   cudaError_t e = cudaErrorInvalidValue;
-#define TATN_BWD_CASE(i, DD, B16, F32) \
-  case i: e = tatn_bwd_launch_t<DD, B16, F32>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches); break;
+#define TATN_BWD_CASE(i, DD, B16, F32, DR) \
+  case i: e = tatn_bwd_launch_t<DD, B16, F32, DR>(d, q, k, v, o, dO, lse, dq, dk, dv, ws, stream, launches); break;
   switch (sel) {
-    TATN_BWD_CASE(0, 64, false, false)
-    TATN_BWD_CASE(1, 64, false, true)
-    TATN_BWD_CASE(2, 64, true, false)
-    TATN_BWD_CASE(3, 64, true, true)
-    TATN_BWD_CASE(4, 128, false, false)
-    TATN_BWD_CASE(5, 128, false, true)
-    TATN_BWD_CASE(6, 128, true, false)
-    TATN_BWD_CASE(7, 128, true, true)
+    TATN_BWD_CASE(0, 64, false, false, false)
+    TATN_BWD_CASE(1, 64, false, false, true)
+    TATN_BWD_CASE(2, 64, false, true, false)
+    TATN_BWD_CASE(3, 64, false, true, true)
+    TATN_BWD_CASE(4, 64, true, false, false)
+    TATN_BWD_CASE(5, 64, true, false, true)
+    TATN_BWD_CASE(6, 64, true, true, false)
+    TATN_BWD_CASE(7, 64, true, true, true)
+    TATN_BWD_CASE(8, 128, false, false, false)
+    TATN_BWD_CASE(9, 128, false, false, true)
+    TATN_BWD_CASE(10, 128, false, true, false)
+    TATN_BWD_CASE(11, 128, false, true, true)
+    TATN_BWD_CASE(12, 128, true, false, false)
+    TATN_BWD_CASE(13, 128, true, false, true)
+    TATN_BWD_CASE(14, 128, true, true, false)
+    TATN_BWD_CASE(15, 128, true, true, true)
   }
 #undef TATN_BWD_CASE
   return e == cudaSuccess ? TATN_OK : TATN_E_CUDA;

@@ -22,7 +22,8 @@
 
 namespace tatn_host {
 int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm = 1);
-}
+}  // namespace tatn_host
+using tatn_host::set_dropout;
 using tatn_host::schedule_group;
 
 namespace {
@@ -108,8 +109,7 @@ int validate(const tatn_attn_desc* d) {
   if (d->dtype != TATN_DTYPE_BF16 && d->dtype != TATN_DTYPE_FP16) return TATN_E_UNSUPPORTED;
   if (d->out_dtype != TATN_OUT_INPUT_DTYPE && d->out_dtype != TATN_OUT_FP32) return TATN_E_UNSUPPORTED;
   if (!(d->tau > 0.f) || !std::isfinite(d->tau)) return TATN_E_ARG;  // attn_config.cpp:52
-  if (!(d->p_drop >= 0.f && d->p_drop < 1.f)) return TATN_E_ARG;      // attn_config.cpp:54
-  if (d->p_drop != 0.f) return TATN_E_UNSUPPORTED;
+  if (!(d->p_drop >= 0.0 && d->p_drop < 1.0)) return TATN_E_ARG;      // attn_config.cpp:54
   if (d->mask_kind != TATN_MASK_NONE && d->mask_kind != TATN_MASK_CAUSAL && d->mask_kind != TATN_MASK_KEY_PADDING)
     return TATN_E_UNSUPPORTED;
   if (d->mask_kind == TATN_MASK_KEY_PADDING && d->valid_len == nullptr) return TATN_E_ARG;
@@ -135,11 +135,11 @@ CUtensorMapDataType tma_dtype(int dtype) {
 #ifndef TATN_FWD_NQ_D64
 #define TATN_FWD_NQ_D64 1  // d = 64: one Q tile per CTA, two CTAs per SM
 #endif
-template <int D, bool BF16, bool OUT_F32, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
+template <int D, bool BF16, bool OUT_F32, bool DROP, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
 cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
   using Cfg = tatn_dev::FwdCfg<D, NQ>;
-  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ>;
+  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ, DROP>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -267,20 +267,30 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.o_sb = d.o_str[0];
   p.o_sh = d.o_str[1];
   p.o_sn = d.o_str[2];
-  const int sel = (d.d == 128 ? 4 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 2 : 0) + (f32 ? 1 : 0);
+  const bool drop = d.p_drop > 0.0;
+  set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
+  const int sel = (d.d == 128 ? 8 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 4 : 0) + (f32 ? 2 : 0) + (drop ? 1 : 0);
   e = cudaErrorInvalidValue;
   cudaEvent_t prof_stop = prof_begin(0, s);
-#define TATN_FWD_CASE(i, DD, B16, F32) \
-  case i: e = launch_fwd<DD, B16, F32>(mq, mk, mv, mo, p, s); break;
+#define TATN_FWD_CASE(i, DD, B16, F32, DR) \
+  case i: e = launch_fwd<DD, B16, F32, DR>(mq, mk, mv, mo, p, s); break;
   switch (sel) {
-    TATN_FWD_CASE(0, 64, false, false)
-    TATN_FWD_CASE(1, 64, false, true)
-    TATN_FWD_CASE(2, 64, true, false)
-    TATN_FWD_CASE(3, 64, true, true)
-    TATN_FWD_CASE(4, 128, false, false)
-    TATN_FWD_CASE(5, 128, false, true)
-    TATN_FWD_CASE(6, 128, true, false)
-    TATN_FWD_CASE(7, 128, true, true)
+    TATN_FWD_CASE(0, 64, false, false, false)
+    TATN_FWD_CASE(1, 64, false, false, true)
+    TATN_FWD_CASE(2, 64, false, true, false)
+    TATN_FWD_CASE(3, 64, false, true, true)
+    TATN_FWD_CASE(4, 64, true, false, false)
+    TATN_FWD_CASE(5, 64, true, false, true)
+    TATN_FWD_CASE(6, 64, true, true, false)
+    TATN_FWD_CASE(7, 64, true, true, true)
+    TATN_FWD_CASE(8, 128, false, false, false)
+    TATN_FWD_CASE(9, 128, false, false, true)
+    TATN_FWD_CASE(10, 128, false, true, false)
+    TATN_FWD_CASE(11, 128, false, true, true)
+    TATN_FWD_CASE(12, 128, true, false, false)
+    TATN_FWD_CASE(13, 128, true, false, true)
+    TATN_FWD_CASE(14, 128, true, true, false)
+    TATN_FWD_CASE(15, 128, true, true, true)
   }
 #undef TATN_FWD_CASE
   if (prof_stop) cudaEventRecord(prof_stop, s);

@@ -63,6 +63,10 @@ struct FwdCfg {
   static constexpr uint32_t kTmemS = 0;
   static constexpr uint32_t kTmemO = NQ * 128;
   static constexpr uint32_t kTmemCols = NQ == 2 ? 512 : 256;  // power of two
+  // P (16-bit, 64 columns per Q tile) gets its own columns when TMEM has room
+  // (d = 64 layouts); otherwise it overwrites the first 64 columns of S.
+  static constexpr bool kSeparateP = (NQ * (128 + D + 64)) <= static_cast<int>(kTmemCols);
+  static constexpr uint32_t kTmemP = kSeparateP ? NQ * (128 + D) : kTmemS;
 };
 
 constexpr int kMaxSparseTiles = 2048;  // tc limit of the block-sparse path (N <= 256K)
@@ -139,7 +143,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
-template <int D, bool BF16, bool OUT_F32, int NQ>
+template <int D, bool BF16, bool OUT_F32, int NQ, bool DROP>
 __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     tatn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -338,7 +342,8 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
 #pragma unroll
           for (int kk = 0; kk < kBN / 16; ++kk) {
             // V tile is MN-major for this product: 16 keys = 2 x 1024B swizzle atoms.
-            mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemS + q * 128 + kk * 8,
+            mma_ts(tmem_base + Cfg::kTmemO + q * D,
+                   tmem_base + Cfg::kTmemP + q * (Cfg::kSeparateP ? 64 : 128) + kk * 8,
                    vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv, (acc[q] | (kk > 0 ? 1u : 0u)));
           }
         }
@@ -398,6 +403,10 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t tS = tmem_base + lane_off + Cfg::kTmemS + q * 128;
     const uint32_t tO = tmem_base + lane_off + Cfg::kTmemO + q * D;
+    const uint32_t tP = tmem_base + lane_off + Cfg::kTmemP + q * (Cfg::kSeparateP ? 64 : 128);
+    // dropout: per-row hash of the reference's positional generator (slice seed = seed + b*H + h)
+    uint64_t drow = 0;
+    if constexpr (DROP) drow = drop_row_hash(p.drop_seed + static_cast<uint64_t>(bh), grow);
     const float sl2 = p.scale_log2;
     const bool causal = p.mask_kind == kMaskCausal;
 
@@ -426,101 +435,150 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
           }
         }
       };
-      // pass 1: row max, streaming S from TMEM in 32-column chunks (3-input max);
-      // the load of chunk c+1 is in flight while chunk c is reduced
-      float mx0 = -INFINITY, mx1 = -INFINITY;
-      {
+      const uint64_t sl2x2 = f2_pack(sl2, sl2);
+      // One streaming pass over S: p = 2^(s*scale_log2 - m_use) per 32-column chunk
+      // (FFMA2 scale, MUFU ex2 or the FMA-pipe polynomial for (i & 7) < kEmuPairs on
+      // full tiles), P (16-bit) to TMEM at tP, row sum in FP32x2; optionally tracks
+      // the raw row max. With aliased P (tP == tS) chunk c lands on S columns
+      // [16c, 16c+16), which the pass has already consumed.
+      auto exp_pass = [&](float m_use, float& raw_max) -> float {
+        const uint64_t negm = f2_pack(-m_use, -m_use);
+        uint64_t rsum0 = f2_pack(0.f, 0.f), rsum1 = rsum0;
+        float mx0 = -INFINITY, mx1 = -INFINITY;
         uint32_t ra[32], rb[32];
         tmem_ld32_async(tS, ra);
         tmem_ld_wait32(ra);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t (&cur)[32] = (c & 1) ? rb : ra;
+          uint32_t (&r)[32] = (c & 1) ? rb : ra;
           uint32_t (&nxt)[32] = (c & 1) ? ra : rb;
           if (c + 1 < 4) tmem_ld32_async(tS + (c + 1) * 32, nxt);
-          apply_mask(cur, c);
+          apply_mask(r, c);
+          if (Cfg::kSeparateP) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            mx0 = fmax3(mx0, __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]));
-            mx1 = fmax3(mx1, __uint_as_float(cur[i + 2]), __uint_as_float(cur[i + 3]));
+            for (int i = 0; i < 32; i += 4) {
+              mx0 = fmax3(mx0, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+              mx1 = fmax3(mx1, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+            }
           }
-          if (c + 1 < 4) tmem_ld_wait32(nxt);
-        }
-      }
-      const float m_tile = fmaxf(mx0, mx1) * sl2;
-      if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(9);
-      float alpha = 1.f;
-      if (m_tile - m_run > kRescaleThreshold) {  // false for NaN (both -inf)
-        alpha = ex2_approx(m_run - m_tile);      // 0 when m_run == -inf
-        m_run = m_tile;
-      }
-      l_run *= alpha;
-      const bool rescale = (n_done > 0) && (alpha != 1.f);
-      if (__any_sync(0xffffffffu, rescale)) {
+          uint32_t pk[16];
+          // straight-line bodies: the polynomial pairs interleave with the MUFU pairs
+          auto exp_chunk = [&](auto emu_on) {
+            constexpr bool kEmu = decltype(emu_on)::value;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + c * 32, o);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(tO + c * 32, o);
-        }
-      }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      // pass 2: p = 2^(s*scale_log2 - m) per 32-column chunk (FFMA2 scale, MUFU ex2 or
-      // the FMA-pipe polynomial for (i & 7) < kEmuPairs on full tiles); P (16-bit)
-      // is stored over S columns [16c, 16c+16), which pass 2 has already consumed.
-      const uint64_t sl2x2 = f2_pack(sl2, sl2), negm = f2_pack(-m_use, -m_use);
-      uint64_t rsum0 = f2_pack(0.f, 0.f), rsum1 = rsum0;
-      uint32_t ra[32], rb[32];
-      tmem_ld32_async(tS, ra);
-      tmem_ld_wait32(ra);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t (&r)[32] = (c & 1) ? rb : ra;
-        uint32_t (&nxt)[32] = (c & 1) ? ra : rb;
-        if (c + 1 < 4) tmem_ld32_async(tS + (c + 1) * 32, nxt);
-        apply_mask(r, c);
-        uint32_t pk[16];
-        // straight-line bodies: the polynomial pairs interleave with the MUFU pairs
-        auto exp_chunk = [&](auto emu_on) {
-          constexpr bool kEmu = decltype(emu_on)::value;
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int i = c * 16 + k;
-            const uint64_t x =
-                f2_fma(f2_pack(__uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1])), sl2x2, negm);
-            uint64_t pv;
-            if constexpr (TATN_EX2_16 && !OUT_F32) {
-              float x0, x1;
-              f2_unpack(x, x0, x1);
-              pk[k] = ex2_pair16<BF16>(x0, x1);
-              pv = widen_pair16<BF16>(pk[k]);  // l sums exactly the P the MMA consumes
-            } else {
-              if (kEmu && (i & 7) < kEmuPairs) {
-                pv = exp2_poly_f2(x);
-              } else {
+            for (int k = 0; k < 16; ++k) {
+              const int i = c * 16 + k;
+              const uint64_t x =
+                  f2_fma(f2_pack(__uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1])), sl2x2, negm);
+              uint64_t pv;
+              if constexpr (TATN_EX2_16 && !OUT_F32 && !DROP) {
                 float x0, x1;
                 f2_unpack(x, x0, x1);
-                pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
+                pk[k] = ex2_pair16<BF16>(x0, x1);
+                pv = widen_pair16<BF16>(pk[k]);  // l sums exactly the P the MMA consumes
+              } else {
+                if (kEmu && (i & 7) < kEmuPairs) {
+                  pv = exp2_poly_f2(x);
+                } else {
+                  float x0, x1;
+                  f2_unpack(x, x0, x1);
+                  pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
+                }
+                float p0, p1;
+                f2_unpack(pv, p0, p1);
+                if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
+                  const int j0 = k0 + c * 32 + 2 * k;
+                  p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
+                  p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
+                }
+                pk[k] = pack2<BF16>(p0, p1);
               }
-              float p0, p1;
-              f2_unpack(pv, p0, p1);
-              pk[k] = pack2<BF16>(p0, p1);
+              if (k & 1) rsum1 = f2_add(rsum1, pv);
+              else rsum0 = f2_add(rsum0, pv);
             }
-            if (k & 1) rsum1 = f2_add(rsum1, pv);
-            else rsum0 = f2_add(rsum0, pv);
+          };
+          // the polynomial needs finite x: full tiles with m_use <= the true max + threshold
+          if (kEmuPairs > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
+          else exp_chunk(std::false_type{});
+          tmem_st16(tP + c * 16, pk);
+          if (c + 1 < 4) tmem_ld_wait32(nxt);
+        }
+        raw_max = fmaxf(mx0, mx1);
+        float rs0, rs1, rs2, rs3;
+        f2_unpack(rsum0, rs0, rs1);
+        f2_unpack(rsum1, rs2, rs3);
+        return (rs0 + rs1) + (rs2 + rs3);
+      };
+      auto rescale_o = [&](float alpha, bool mine) {
+        if (__any_sync(0xffffffffu, mine)) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + c * 32, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tO + c * 32, o);
           }
-        };
-        if (kEmuPairs > 0 && !need_mask) exp_chunk(std::true_type{});
-        else exp_chunk(std::false_type{});
-        tmem_st16(tS + c * 16, pk);
-        if (c + 1 < 4) tmem_ld_wait32(nxt);
+        }
+      };
+      float row_sum = 0.f;
+      bool settled = false;
+      if (Cfg::kSeparateP && n_done > 0 && __all_sync(0xffffffffu, m_run != -INFINITY)) {
+        // optimistic single pass against the running max; redo only if the max jumped
+        // past the lazy-rescale threshold (the polynomial clamps overflowing inputs, and
+        // such a pass is discarded)
+        float raw_max;
+        row_sum = exp_pass(m_run, raw_max);
+        const float m_tile = raw_max * sl2;
+        const bool jumped = m_tile - m_run > kRescaleThreshold;
+        settled = !__any_sync(0xffffffffu, jumped);
+        if (!settled) {  // warp-uniform branch: TMEM ld/st below are .sync.aligned
+          float alpha = 1.f;
+          if (jumped) {
+            alpha = ex2_approx(m_run - m_tile);
+            m_run = m_tile;
+            l_run *= alpha;
+          }
+          rescale_o(alpha, jumped);
+        }
       }
-      float rs0, rs1, rs2, rs3;
-      f2_unpack(rsum0, rs0, rs1);
-      f2_unpack(rsum1, rs2, rs3);
-      l_run += (rs0 + rs1) + (rs2 + rs3);
+      if (!settled) {
+        float m_tile;
+        if (Cfg::kSeparateP && n_done > 0 && __all_sync(0xffffffffu, m_run != -INFINITY)) {
+          m_tile = m_run;  // already advanced above
+        } else {
+          // pass 1: row max, streaming S from TMEM in 32-column chunks (3-input max)
+          float mx0 = -INFINITY, mx1 = -INFINITY;
+          uint32_t ra[32], rb[32];
+          tmem_ld32_async(tS, ra);
+          tmem_ld_wait32(ra);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t (&cur)[32] = (c & 1) ? rb : ra;
+            uint32_t (&nxt)[32] = (c & 1) ? ra : rb;
+            if (c + 1 < 4) tmem_ld32_async(tS + (c + 1) * 32, nxt);
+            apply_mask(cur, c);
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              mx0 = fmax3(mx0, __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]));
+              mx1 = fmax3(mx1, __uint_as_float(cur[i + 2]), __uint_as_float(cur[i + 3]));
+            }
+            if (c + 1 < 4) tmem_ld_wait32(nxt);
+          }
+          m_tile = fmaxf(mx0, mx1) * sl2;
+          float alpha = 1.f;
+          if (m_tile - m_run > kRescaleThreshold) {  // false for NaN (both -inf)
+            alpha = ex2_approx(m_run - m_tile);      // 0 when m_run == -inf
+            m_run = m_tile;
+          }
+          l_run *= alpha;
+          rescale_o(alpha, (n_done > 0) && (alpha != 1.f));
+        }
+        if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(9);
+        float unused;
+        row_sum = exp_pass((m_run == -INFINITY) ? 0.f : m_run, unused);
+      }
+      l_run += row_sum;
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(BAR(kBarPFull + q));

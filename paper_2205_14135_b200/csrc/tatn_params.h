@@ -20,6 +20,9 @@ struct FwdParams {
   float* lse;                // [B, H, Nq] natural-log logsumexp (fp32)
   int n_pairs;               // ceil(Nq / 256): CTAs per (b, h)
   int group;                 // heads per scheduling group (CTA order, see tatn_fwd_kernel)
+  uint64_t drop_seed;        // dropout: slice (b, h) uses mix64 chains from drop_seed + b*H + h
+  uint64_t drop_thresh;      // keep iff hash >= drop_thresh  (= ceil(p * 2^53) << 11)
+  float drop_scale;          // 1 / (1 - p)
   float* o_f32;              // fp32 output mode: O written here directly (strides below)
   int64_t o_sb, o_sh, o_sn;
 };
@@ -38,6 +41,9 @@ struct BwdParams {
   float* dq_acc;     // [B, H, Nq, d] fp32 workspace
   int n_ktiles;      // ceil(Nk / 128)
   int group;         // heads per scheduling group (CTA order, see tatn_bwd_kernel)
+  uint64_t drop_seed;   // dropout (see FwdParams)
+  uint64_t drop_thresh;
+  float drop_scale;
   float* dk_f32;     // fp32 output mode: dK / dV written directly (strides below)
   float* dv_f32;
   int64_t k_sb, k_sh, k_sn, v_sb, v_sh, v_sn;

@@ -266,8 +266,8 @@ int main() {
       const TilePlan plan = plan_tiles(n, d, 65536);
       MemoryModel mem(plan.m_capacity);
       AttnConfig drop = AttnConfig::make(n, d);
-      drop.p_drop = 0.1;
-      report("error_dropout_unsupported", throws([&] { flash_forward(x, x, x, drop, plan, mem); }));
+      drop.p_drop = 1.0;
+      report("error_dropout_p_out_of_range", throws([&] { flash_forward(x, x, x, drop, plan, mem); }));
       AttnConfig cust = AttnConfig::make(n, d);
       cust.mask = MaskSpec::custom_additive(Matrix(n, n));
       report("error_custom_mask_unsupported", throws([&] { flash_forward(x, x, x, cust, plan, mem); }));
@@ -287,6 +287,27 @@ int main() {
       const TilePlan p64 = plan_tiles(n, d, 65536, ov);
       report("error_block_size_not_multiple_of_128",
              throws([&] { blocksparse_forward(x, x, x, ok, p64, b64, mem); }));
+    }
+
+    // ---- dropout: same positional mask as the reference (dropout.cpp)
+    for (double pd : {0.1, 0.5}) {
+      const size_t n = 300, d = 64;
+      AttnConfig cfg = AttnConfig::make(n, d);
+      cfg.mask = MaskSpec::causal();
+      cfg.p_drop = pd;
+      cfg.seed = 7;
+      Matrix q = rounded(gaussian_matrix(n, d, 71)), k = rounded(gaussian_matrix(n, d, 72)),
+             v = rounded(gaussian_matrix(n, d, 73)), dO = rounded(gaussian_matrix(n, d, 74));
+      const TilePlan plan = plan_tiles(n, d, 116224);
+      MemoryModel mem(plan.m_capacity);
+      FlashSaved s = flash_forward(q, k, v, cfg, plan, mem);
+      ForwardArtifacts r = standard_forward(q, k, v, cfg);
+      Gradients g = flash_backward(s, q, k, v, dO, mem);
+      Gradients rg = standard_backward(r, q, k, v, dO, cfg);
+      const std::string tag = "dropout_p" + std::to_string(static_cast<int>(pd * 10));
+      report(tag + "_forward", close(s.o, r.o), fmt(max_abs(s.o, r.o), rel_l2(s.o, r.o)));
+      report(tag + "_backward", close(g.dq, rg.dq) && close(g.dk, rg.dk) && close(g.dv, rg.dv),
+             fmt(max_abs(g.dv, rg.dv), rel_l2(g.dv, rg.dv)));
     }
 
     // ---- fp16 input mode

@@ -14,9 +14,11 @@
 //   * charge the MemoryModel with the exact element counts of the reference's
 //     tiled schedule for `plan` (io_predict.hpp counting rules, per visited
 //     block for the block-sparse engines) and lease plan.working_set.
-// There is no CPU fallback: unsupported inputs (Custom n x n masks, dropout,
-// d > 128, block sizes that are not multiples of 128) throw, and a missing
-// sm_100 device surfaces as std::runtime_error.
+// Dropout follows the reference's positional generator bit for bit (the mask at
+// (i, j) is a pure function of (seed, i, j), dropout.hpp:14-30), so forward and
+// backward regenerate identical masks. There is no CPU fallback: unsupported
+// inputs (Custom n x n masks, d > 128, block sizes that are not multiples of
+// 128) throw, and a missing sm_100 device surfaces as std::runtime_error.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -145,8 +147,6 @@ void check_inputs(const char* op, const Matrix& q, const Matrix& k, const Matrix
   if (has_nan(q) || has_nan(k) || has_nan(v)) throw std::invalid_argument(std::string(op) + ": NaN input");
   if (cfg.mask.kind == MaskKind::Custom)
     throw std::invalid_argument(std::string(op) + ": Custom n x n masks are not supported on the sm_100a path");
-  if (cfg.p_drop != 0.0)
-    throw std::invalid_argument(std::string(op) + ": dropout (p_drop != 0) is not supported on the sm_100a path");
 }
 
 void check_plan(const char* op, const TilePlan& plan, std::size_t n, std::size_t d) {
@@ -182,6 +182,8 @@ Problem make_problem(const Matrix& q, const Matrix& k, const AttnConfig& cfg) {
                                                         : TATN_MASK_NONE;
   d.tr = static_cast<int32_t>((P.n + 127) / 128);
   d.tc = static_cast<int32_t>((P.nk + 127) / 128);
+  d.p_drop = cfg.p_drop;  // one head per call: slice 0 uses cfg.seed, i.e. the reference's mask
+  d.seed = cfg.seed;
   return P;
 }
 

@@ -29,7 +29,10 @@ CASES = [
     ("prefix_causal_bf16_d128", 1, 1, 256, 160, 128, "bf16", "causal", None, None),
     ("butterfly_bf16_d64", 1, 1, 512, 512, 64, "bf16", "none", None, "butterfly"),
     ("sparse_emptyrow_causal_bf16_d64", 1, 1, 384, 384, 64, "bf16", "causal", None, "emptyrow"),
+    # dropout p = 0.2, seed 1234 (slice (b, h) uses seed + b*H + h, the C ABI's batched convention)
+    ("dropout_causal_bf16_d64", 1, 2, 192, 192, 64, "bf16", "causal", None, None),
 ]
+DROPOUT = {"dropout_causal_bf16_d64": (0.2, 1234)}
 
 
 def grid_for(kind, tr, tc):
@@ -68,8 +71,10 @@ def main():
         res = {key: [] for key in ("o", "lse", "dq", "dk", "dv")}
         for b in range(B):
             for h in range(H):
+                pd, sd = DROPOUT.get(name, (0.0, 0))
                 r = O.ref_standard(q[b, h], k[b, h], v[b, h], do[b, h], mask=mask,
-                                   valid_len=(vl[b] if vl is not None else None), grid=grid, br=128, bc=128)
+                                   valid_len=(vl[b] if vl is not None else None), grid=grid, br=128, bc=128,
+                                   p_drop=pd, seed=sd + b * H + h)
                 for key in res:
                     res[key].append(r[key])
         for key in res:
@@ -81,7 +86,8 @@ def main():
             out[f"{name}/grid"] = grid
         if vl is not None:
             out[f"{name}/valid_len"] = np.asarray(vl, dtype=np.int32)
-        meta.append(dict(name=name, B=B, H=H, Nq=Nq, Nk=Nk, d=d, dtype=dt, mask=mask,
+        pd, sd = DROPOUT.get(name, (0.0, 0))
+        meta.append(dict(name=name, B=B, H=H, Nq=Nq, Nk=Nk, d=d, dtype=dt, mask=mask, p_drop=pd, seed=sd,
                          has_grid=grid is not None, has_valid_len=vl is not None))
     out["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
     np.savez_compressed(ROOT / "tests" / "golden" / "attn_golden.npz", **out)

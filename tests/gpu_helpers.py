@@ -32,10 +32,10 @@ def empty_like_layout(t: torch.Tensor, dtype=None) -> torch.Tensor:
 
 
 def run_gpu(q, k, v, do, dtype, mask="none", valid_len=None, grid=None, backward=True, layout="bhnd",
-            visited=False, out_fp32=False):
+            visited=False, out_fp32=False, p_drop=0.0, seed=0):
     """Forward (+ backward) on the device through the C ABI. Returns numpy fp64 outputs."""
     qd, kd, vd = (to_dev(t, dtype, layout) for t in (q, k, v))
-    spec = A.AttnSpec(mask=mask, out_fp32=out_fp32)
+    spec = A.AttnSpec(mask=mask, out_fp32=out_fp32, p_drop=p_drop, seed=seed)
     if valid_len is not None:
         spec.valid_len = torch.as_tensor(np.asarray(valid_len, dtype=np.int32)).cuda()
     if grid is not None:
@@ -94,11 +94,12 @@ def assert_close(name, got, ref, max_abs=MAX_ABS, rel_l2=REL_L2):
     return mx, rel
 
 
-def oracle_full(q, k, v, do, mask="none", valid_len=None, grid=None, backward=True):
-    o, lse = O.forward(q, k, v, mask=mask, valid_len=valid_len, grid=grid)
+def oracle_full(q, k, v, do, mask="none", valid_len=None, grid=None, backward=True, p_drop=0.0, seed=0):
+    o, lse = O.forward(q, k, v, mask=mask, valid_len=valid_len, grid=grid, p_drop=p_drop, seed=seed)
     out = {"o": o, "lse": lse}
     if backward:
-        dq, dk, dv = O.backward(q, k, v, o, do, lse, mask=mask, valid_len=valid_len, grid=grid)
+        dq, dk, dv = O.backward(q, k, v, o, do, lse, mask=mask, valid_len=valid_len, grid=grid, p_drop=p_drop,
+                                seed=seed)
         out.update(dq=dq, dk=dk, dv=dv)
     return out
 

@@ -40,7 +40,7 @@ def test_exports_have_c_linkage():
 
 def test_abi_version_and_strerror():
     lib = _lib.load()
-    assert lib.tatn_abi_version() == 1
+    assert lib.tatn_abi_version() == 2
     for code in range(7):
         assert _lib.strerror(code)
     assert _lib.strerror(99) == "unknown status"
@@ -81,7 +81,7 @@ def test_valid_descriptor_passes():
         (dict(tau=float("inf")), _lib.TATN_E_ARG),
         (dict(tau=float("nan")), _lib.TATN_E_ARG),
         (dict(p_drop=1.0), _lib.TATN_E_ARG),  # p in [0, 1) (attn_config.cpp:54)
-        (dict(p_drop=0.1), _lib.TATN_E_UNSUPPORTED),  # dropout is not on the device path
+        (dict(p_drop=-0.1), _lib.TATN_E_ARG),
         (dict(mask_kind=3), _lib.TATN_E_UNSUPPORTED),  # Custom n x n masks
         (dict(mask_kind=_lib.TATN_MASK_KEY_PADDING), _lib.TATN_E_ARG),  # no valid_len
     ],

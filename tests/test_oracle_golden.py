@@ -55,14 +55,15 @@ def test_generator_matches_golden_seeds():
             assert np.array_equal(O.gaussian_matrix(8, 8, seed), g[key])
 
 
-@pytest.mark.parametrize("idx", range(6))
+@pytest.mark.parametrize("idx", range(7))
 def test_oracle_matches_golden(idx):
     z, meta = load_cases()
     m = meta[idx]
     q, k, v, do, grid, vl = case_inputs(z, m)
     name = m["name"]
-    o, lse = O.forward(q, k, v, mask=m["mask"], valid_len=vl, grid=grid)
-    dq, dk, dv = O.backward(q, k, v, o, do, lse, mask=m["mask"], valid_len=vl, grid=grid)
+    pd, sd = m.get("p_drop", 0.0), m.get("seed", 0)
+    o, lse = O.forward(q, k, v, mask=m["mask"], valid_len=vl, grid=grid, p_drop=pd, seed=sd)
+    dq, dk, dv = O.backward(q, k, v, o, do, lse, mask=m["mask"], valid_len=vl, grid=grid, p_drop=pd, seed=sd)
     gl = z[f"{name}/lse"].astype(np.float64)
     assert np.array_equal(np.isneginf(lse), np.isneginf(gl))
     fin = np.isfinite(gl)

@@ -92,3 +92,28 @@ def test_standard_counters_equal_closed_forms():
         assert tuple(int(c) for c in r["bwd_counters"][:2]) == O.predict_io("standard_backward", n, d)
         assert int(r["fwd_counters"][2]) == O.flop_model(0, n, d)
         assert int(r["bwd_counters"][2]) == O.flop_model(1, n, d)
+
+
+def test_dropout_generator_bit_exact():
+    # dropout.cpp:7-27: the oracle's restatement of the positional PRNG equals the reference's
+    rng = np.random.default_rng(9)
+    for _ in range(300):
+        seed = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
+        i, j = int(rng.integers(0, 1 << 20)), int(rng.integers(0, 1 << 20))
+        p = float(rng.choice([0.0, 0.1, 0.5, 0.9, float(rng.random())]))
+        assert O.dropout_scale(seed, i, j, p) == O.ref_dropout_scale(seed, i, j, p)
+
+
+@pytest.mark.parametrize("p_drop,seed,mask", [(0.1, 7, "none"), (0.5, 3, "causal"), (0.2, 2**40 + 1, "key_padding")])
+def test_dropout_matches_reference(p_drop, seed, mask):
+    # flash == standard with the same seed (here: the oracle == the reference)
+    rng = np.random.default_rng(11)
+    n, d = 90, 8
+    vl = 61 if mask == "key_padding" else None
+    q, k, v, do = (rng.standard_normal((n, d)) for _ in range(4))
+    r = O.ref_standard(q, k, v, do, mask=mask, valid_len=vl, p_drop=p_drop, seed=seed)
+    o, lse = O.forward(q[None, None], k[None, None], v[None, None], mask=mask, valid_len=vl, p_drop=p_drop, seed=seed)
+    dq, dk, dv = O.backward(q[None, None], k[None, None], v[None, None], o, do[None, None], lse, mask=mask,
+                            valid_len=vl, p_drop=p_drop, seed=seed)
+    for a, b in ((o, r["o"]), (dq, r["dq"]), (dk, r["dk"]), (dv, r["dv"])):
+        np.testing.assert_allclose(a[0, 0], b, rtol=0, atol=1e-10)

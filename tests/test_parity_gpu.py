@@ -31,7 +31,7 @@ def _golden():
     return z, json.loads(bytes(z["meta"]).decode())
 
 
-@pytest.mark.parametrize("idx", range(6))
+@pytest.mark.parametrize("idx", range(7))
 def test_golden_fixture(cuda_device, idx):
     z, meta = _golden()
     m = meta[idx]
@@ -46,7 +46,8 @@ def test_golden_fixture(cuda_device, idx):
     q, k, v, do = dec("q"), dec("k"), dec("v"), dec("do")
     grid = z[f"{name}/grid"] if m["has_grid"] else None
     vl = z[f"{name}/valid_len"] if m["has_valid_len"] else None
-    got = G.run_gpu(q, k, v, do, m["dtype"], mask=m["mask"], valid_len=vl, grid=grid, visited=grid is not None)
+    got = G.run_gpu(q, k, v, do, m["dtype"], mask=m["mask"], valid_len=vl, grid=grid, visited=grid is not None,
+                    p_drop=m.get("p_drop", 0.0), seed=m.get("seed", 0))
     ref = {key: z[f"{name}/{key}"].astype(np.float64) for key in ("o", "lse", "dq", "dk", "dv")}
     compare_all(got, ref)
     if grid is not None:
@@ -244,3 +245,31 @@ def test_error_codes_surface(cuda_device):
     assert e.value.status == _lib.TATN_E_ARG
     with pytest.raises(TypeError):
         A.flash_fwd(q.float(), q.float(), q.float())
+
+
+# ----------------------------------------------------------------------------- dropout
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("p_drop,mask", [(0.1, "causal"), (0.5, "none"), (0.3, "key_padding")])
+def test_dropout_parity(cuda_device, d, p_drop, mask):
+    # same positional mask as the reference (dropout.cpp), regenerated in the backward
+    vl = np.array([333, 64], dtype=np.int32) if mask == "key_padding" else None
+    q, k, v, do = G.make_inputs(2, 3, 333, 333, d, "bf16")
+    got = G.run_gpu(q, k, v, do, "bf16", mask=mask, valid_len=vl, out_fp32=True, p_drop=p_drop, seed=99)
+    compare_all(got, G.oracle_full(q, k, v, do, mask=mask, valid_len=vl, p_drop=p_drop, seed=99))
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_dropout_mask_bit_exact(cuda_device, d):
+    # Q = K = 0 makes every P_ij = 1/N, so with V = I the forward output is O = Z / N
+    # (Z = the dropout scale matrix) and with dO = I the backward gives dV^T = Z / N:
+    # the zero pattern of O and of dV^T is the kept/dropped mask itself, bit for bit.
+    N, p_drop, seed = d, 0.4, 2**40 + 3
+    B, H = 1, 2
+    zeros = np.zeros((B, H, N, d))
+    eye = np.broadcast_to(np.eye(N, d), (B, H, N, d)).copy()
+    got = G.run_gpu(zeros, zeros, eye, eye, "bf16", p_drop=p_drop, seed=seed, out_fp32=True)
+    for h in range(H):
+        ref = np.array([[O.dropout_scale(seed + h, i, j, p_drop) for j in range(N)] for i in range(N)])
+        assert np.array_equal(got["o"][0, h] != 0, ref != 0), "forward mask differs"
+        assert np.array_equal(got["dv"][0, h].T != 0, ref != 0), "backward mask differs"
+        np.testing.assert_allclose(got["o"][0, h], ref / N, rtol=4e-3)  # P/(1-p) is rounded to bf16 for the MMA
