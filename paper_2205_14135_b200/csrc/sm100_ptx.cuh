@@ -320,6 +320,11 @@ __device__ __forceinline__ uint64_t f2_add_rm(uint64_t a, uint64_t b) {
   asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("sub.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -398,5 +403,23 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                "r"(d)
                : "memory");
 }
+
+// ---- per-CTA globaltimer trace (debug builds only: -DTATN_TRACE)
+#ifdef TATN_TRACE
+__device__ unsigned long long* g_tatn_trace = nullptr;  // [grid][8] globaltimer stamps (debug builds only)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TATN_TRACE_AT(slot)                                                                     \
+  do {                                                                                          \
+    if (g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + (slot)] = gtimer();   \
+  } while (0)
+#else
+#define TATN_TRACE_AT(slot) \
+  do {                      \
+  } while (0)
+#endif
 
 }  // namespace tatn_dev

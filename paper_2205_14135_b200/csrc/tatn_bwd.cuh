@@ -8,26 +8,29 @@
 // the outer loop (one CTA per 128-key tile) and dQ is a read-modify-write
 // accumulation — here an fp32 bulk reduce-add into an L2-resident workspace.
 //
-//   K2 tatn_bwd_pre   : D_i, lse2_i = LSE_i*log2(e) (+inf for empty/padded rows), zero dQacc
+//   K2 tatn_bwd_pre   : -D_i, -lse2_i = -LSE_i*log2(e) (-inf for empty/padded rows), zero dQacc
 //   K3 tatn_bwd_kernel: per (b, h, key tile) loop over 64-row Q tiles
 //   K4 tatn_bwd_post  : dQ = bf16/fp16(dQacc)
 //
-// K3 CTA layout (320 threads):
-//   warps 0-3 "softmax": thread = key row (TMEM lane). Recompute P^T, dS^T.
-//   warps 4-7 "dQ":      thread = head-dim row of dQ^T (TMEM lane); stage + bulk reduce.
-//   warp  8   TMA producer (K, V once; Q_i, dO_i, lse2_i, D_i ring)
-//   warp  9   TMEM allocator + tcgen05.mma issuer
+// K3 CTA layout (448 threads):
+//   warps 0-3 "softmax 0": thread = key row (TMEM lane). Recompute P^T, dS^T for even Q tiles.
+//   warps 4-7 "softmax 1": the same for odd Q tiles (ping-pong: two tiles in softmax at once).
+//   warps 8-11 "dQ":       thread = head-dim row of dQ^T (TMEM lane); stage + bulk reduce.
+//   warp 12   TMA producer (K, V once; Q_i, dO_i, lse2_i, D_i ring)
+//   warp 13   TMEM allocator + tcgen05.mma issuer
 // Per Q tile i the MMA computes (M = 128 keys unless noted)
 //   front: S^T = K Q_i^T, dP^T = V dO_i^T                      (N = 64 queries)
 //   back : dV += P^T dO_i, dK += dS^T Q_i  (A from TMEM)       (N = d)
 //          dQ_i^T = K^T dS^T  (M = d rows used, A/B from SMEM) (N = 64 queries)
-// with two TMEM buffers X0/X1 holding {S^T | dP^T} so that front(i+1)
-// overlaps softmax(i) and back(i) overlaps softmax(i+1).
+// with two TMEM buffers X0/X1 holding {S^T | dP^T}, one per softmax warpgroup.
+// dS is kept unscaled (tau is applied to dK in the epilogue and to dQ in the dQ
+// warpgroup), so the softmax step is P = 2^(S*tau*log2e - lse2), dS = P*(dP - D).
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 
 #include "../../include/tatn_b200.h"
 #include "sm100_ptx.cuh"
@@ -35,17 +38,18 @@
 
 namespace tatn_dev {
 
-constexpr int kBwdThreads = 320;
+constexpr int kBwdThreads = 448;
 constexpr int kBwdQT = 64;    // query rows per Q tile
 constexpr int kBwdKT = 128;   // keys per CTA
 
-template <int D>
+template <int D, bool DROP = false>
 struct BwdCfg {
   static constexpr int kSubs = D / 64;
   static constexpr int kKVTile = kSubs * 128 * 128;   // 128 rows x D x 2B
   static constexpr int kQSub = 64 * 128;              // 64 rows x 128B
   static constexpr int kQTile = kSubs * kQSub;        // 64 rows x D x 2B
-  static constexpr int kStages = (D == 128) ? 3 : 4;
+  // d = 128 with dropout drops to 2 stages to make room for the per-warpgroup row hashes
+  static constexpr int kStages = (D == 128) ? (DROP ? 2 : 3) : 4;
   static constexpr int kDSBytes = 128 * 128;          // 128 keys x 64 q x 2B
   static constexpr int kDQBytes = kBwdQT * D * 4;     // fp32 staging
   static constexpr int kVecBytes = 2 * kBwdQT * 4;    // lse2 + D
@@ -58,11 +62,16 @@ struct BwdCfg {
   static constexpr int kOffVec = kOffDQ + kDQBytes;
   static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
   static constexpr int kOffMask = kOffBar + 256;       // block-sparse q-tile bitmask, 128 words
-  static constexpr int kOffDrop = kOffMask + 512;      // dropout: 64 query-row hashes of the current tile
-  static constexpr int kSmemBytes = kOffDrop + 512;   // dynamic smem is declared __align__(1024)
+  static constexpr int kOffDrop = kOffMask + 512;      // dropout: 64 query-row hashes per softmax warpgroup
+  static constexpr int kSmemBytes = kOffDrop + (DROP ? 1024 : 0);  // dynamic smem is declared __align__(1024)
+  static_assert(kSmemBytes <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
   static constexpr uint32_t kTmemX = 0;    // X_x = x*128: S^T [0,64) dP^T [64,128)
   static constexpr uint32_t kTmemDV = 256;
   static constexpr uint32_t kTmemDK = 256 + D;
+  // d = 64 leaves 128 TMEM columns free: dQ^T gets its own two buffers there, so the next
+  // front (S^T into X_x) need not wait for the dQ warpgroup to drain dQ^T out of X_x.
+  static constexpr bool kSepDQ = (D == 64);
+  static constexpr uint32_t kTmemDQ = 384;  // [384 + 64x, 448 + 64x) when kSepDQ
 };
 
 struct BwdSched {
@@ -176,13 +185,13 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_,
 #pragma unroll
   for (int off = kChunks / 2; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
   if (row < total && c == 0) {
-    delta[row] = part;
-    float l2 = INFINITY;  // P = 0 for padded or fully-masked rows
+    delta[row] = -part;    // stored negated: the softmax step adds it
+    float nl2 = -INFINITY;  // P = 0 for padded or fully-masked rows
     if (qi < Nq) {
       const float l = lse[bh * Nq + qi];
-      if (l != -INFINITY) l2 = l * 1.4426950408889634f;
+      if (l != -INFINITY) nl2 = -l * 1.4426950408889634f;
     }
-    lse2[row] = l2;
+    lse2[row] = nl2;
   }
 }
 
@@ -223,8 +232,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
                     const BwdParams p, const float* __restrict__ lse2, int Nq_pad) {
-  using Cfg = BwdCfg<D>;
+  using Cfg = BwdCfg<D, DROP>;
   constexpr int S = Cfg::kStages;
+  constexpr int kProducerWarp = 12, kMmaWarp = 13;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // 128B-swizzle atoms need 1024B alignment
   const uint32_t smem_base = smem_u32(smem_raw);
@@ -268,6 +278,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int b = bh / p.H;
   const int h = bh - b * p.H;
   uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
+  if (threadIdx.x == 0) TATN_TRACE_AT(0);
 
   if (threadIdx.x == 0) {
     mbar_init(BAR(kBarKV), 1);
@@ -285,13 +296,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(BAR(kBarFinal), 1);
     fence_mbar_init();
   }
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_relinquish();
   }
   BwdSched sc = make_bwd_sched(p, b, j);
   sc.mask = mask_smem;
-  if (sc.gcol != nullptr && warp == 8) {
+  if (sc.gcol != nullptr && warp == kProducerWarp) {
     // block-sparse: read grid column j once into a bitmask over 64-row Q tiles
     for (int base = 0; base < p.tr; base += 32) {
       const int r = base + lane;
@@ -307,8 +318,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // number of Q tiles this key tile visits (same order for every role)
+  int n_iter = 0;
+  for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) ++n_iter;
 
-  if (warp == 8) {
+  if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
     // whole warp runs the loop (waits), one elected lane issues
     if (elect_one_sync()) {
@@ -351,7 +365,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ph ^= 1;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     // whole warp runs the schedule (waits); one elected lane issues tcgen05.mma/commit
     constexpr uint32_t ab = BF16 ? 1u : 0u;
@@ -367,13 +381,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint64_t dDOmn0 = make_sdesc_sw128(sDO, Cfg::kQSub, 1024);     // dO as MN-major B
     const uint64_t dKmn0 = make_sdesc_sw128(sK, 128 * 128, 1024);        // K^T as MN-major A
     const uint64_t dDS0 = make_sdesc_sw128(sDS, 128 * 128, 1024);        // dS^T as MN-major B
-    // list the Q tiles once (the order the producer and consumers use)
-    int n = 0;
-    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) ++n;
+    const int n = n_iter;
     mbar_wait(BAR(kBarKV), 0);
     tc_fence_after();
+    if (lane == 0) TATN_TRACE_AT(1);
+#ifdef TATN_TRACE
+    if (lane == 0 && g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 6] = n;
+#endif
     uint32_t qph = 0;  // phase bit per Q/dO stage (bit s)
-    uint32_t pph[2] = {0, 0}, eph[2] = {0, 0};
+    uint32_t pph = 0, eph = 0;  // phase bits per X buffer (bit x)
 
     auto front_dp = [&](int idx) {
       const int s = idx % S;
@@ -415,9 +431,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int idx = 0; idx < n; ++idx) {
       const int x = idx & 1;
       const int s = idx % S;
-      mbar_wait(BAR(kBarPFull + x), pph[x]);
-      pph[x] ^= 1;
+      mbar_wait(BAR(kBarPFull + x), (pph >> x) & 1u);
+      pph ^= 1u << x;
       tc_fence_after();
+      if (lane == 0 && idx == 2) TATN_TRACE_AT(11);
       const uint32_t accf = idx > 0 ? 1u : 0u;
       if (elect_one_sync()) {
         // dV += P^T dO   (P^T bf16 in X_x cols [0,32); dO MN-major, 16 queries per step)
@@ -430,173 +447,232 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int kk = 0; kk < kBwdQT / 16; ++kk)
           mma_ts(tmem_base + Cfg::kTmemDK, tmem_base + Cfg::kTmemX + x * 128 + 64 + kk * 8,
                  dQmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc, accf | (kk > 0 ? 1u : 0u));
-        // dQ^T = K^T dS^T  (K MN-major as A; dS^T MN-major as B; 16 keys per step) -> X_x cols [0,64)
-#pragma unroll
-        for (int kk = 0; kk < kBwdKT / 16; ++kk)
-          mma_ss(tmem_base + Cfg::kTmemX + x * 128, dKmn0 + ((kk * 2048) >> 4),
-                 dDS0 + (((idx & 1) * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq, kk > 0 ? 1u : 0u);
-        mma_commit(BAR(kBarDQFull + x));
-        mma_commit(BAR(kBarQEmpty + s));
-        mma_commit(BAR(kBarDSEmpty + (idx & 1)));
       }
       __syncwarp();
-      if (idx + 2 < n) {
-        front_dp(idx + 2);  // dP^T region free: its dS^T was consumed above (in-order)
-        mbar_wait(BAR(kBarDQEmpty + x), eph[x]);  // dQ^T of this tile read out of X_x
-        eph[x] ^= 1;
-        tc_fence_after();
-        front_s(idx + 2);
+      auto issue_dq = [&]() {
+        // dQ^T = K^T dS^T  (K MN-major as A; dS^T MN-major as B; 16 keys per step)
+        const uint32_t tDQ = tmem_base + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
+        if (elect_one_sync()) {
+#pragma unroll
+          for (int kk = 0; kk < kBwdKT / 16; ++kk)
+            mma_ss(tDQ, dKmn0 + ((kk * 2048) >> 4), dDS0 + ((x * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq,
+                   kk > 0 ? 1u : 0u);
+          mma_commit(BAR(kBarDQFull + x));
+          mma_commit(BAR(kBarQEmpty + s));
+          mma_commit(BAR(kBarDSEmpty + x));
+        }
+        __syncwarp();
+      };
+      if constexpr (Cfg::kSepDQ) {
+        // X_x is free once dV/dK have read P^T / dS^T (in-order pipe): start the next front
+        // first so S^T(idx + 2) reaches the softmax warpgroup one dQ^T earlier
+        if (idx + 2 < n) {
+          front_dp(idx + 2);
+          front_s(idx + 2);
+        }
+        if (idx >= 2) {
+          mbar_wait(BAR(kBarDQEmpty + x), (eph >> x) & 1u);  // dQ^T(idx - 2) drained from buffer x
+          eph ^= 1u << x;
+          tc_fence_after();
+        }
+        issue_dq();
+      } else {
+        issue_dq();  // dQ^T lands in X_x cols [0,64): the next front waits for the dQ warpgroup
+        if (idx + 2 < n) {
+          front_dp(idx + 2);
+          mbar_wait(BAR(kBarDQEmpty + x), (eph >> x) & 1u);
+          eph ^= 1u << x;
+          tc_fence_after();
+          front_s(idx + 2);
+        }
       }
     }
     if (elect_one_sync()) mma_commit(BAR(kBarFinal));
     __syncwarp();
-  } else if (warp < 4) {
-    // ------------------------------------------------------------ softmax warpgroup
-    const int r = warp * 32 + lane;  // key row within tile == TMEM lane
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int sg = warp >> 2;               // warpgroup = X buffer = parity of its Q tiles
+    const int r = (warp & 3) * 32 + lane;   // key row within tile == TMEM lane
     const int kj = sc.k0 + r;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const float sl2 = p.scale_log2;
-    const float tau = p.tau;
+    const uint64_t sl2x2 = f2_pack(sl2, sl2);
     const bool causal = p.mask_kind == kMaskCausal;
-    uint32_t sph[2] = {0, 0};
-    uint32_t dsph[2] = {0, 0};
-    uint32_t qph = 0;  // phase bit per Q/dO stage (bit s)
+    uint32_t sph = 0, dsph = 0;
+    const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + sg * 128;
+    uint64_t* drop_rows = reinterpret_cast<uint64_t*>(smem_gen + Cfg::kOffDrop + sg * 512);
     int idx = 0;
-    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
-      const int x = idx & 1;
+    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1), ++idx) {
+      if ((idx & 1) != sg) continue;
       const int s = idx % S;
       if (p.visited != nullptr && r == 0) {
         const long long bit = static_cast<long long>(i >> 1) * p.tc + j;
         atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
       }
-      mbar_wait(BAR(kBarQFull + s), (qph >> s) & 1u);  // lse2 / D vectors landed
-      qph ^= 1u << s;
-      mbar_wait(BAR(kBarSFull + x), sph[x]);
-      sph[x] ^= 1;
+      mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>(idx / S) & 1u);  // lse2 / D vectors landed
+      mbar_wait(BAR(kBarSFull + sg), sph);
+      sph ^= 1;
       tc_fence_after();
-      const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + x * 128;
-      uint32_t sr[64], dp[64];
-      tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld32(tX + 64, *reinterpret_cast<uint32_t(*)[32]>(&dp[0]));
-      tmem_ld32(tX + 96, *reinterpret_cast<uint32_t(*)[32]>(&dp[32]));
-      const float* vl = vec_gen + s * (Cfg::kVecBytes / 4);
+      if (r == 0 && idx == 0) TATN_TRACE_AT(2);
+      if (r == 0 && idx == 2) TATN_TRACE_AT(9);
+      const uint64_t* nl2 = reinterpret_cast<const uint64_t*>(vec_gen + s * (Cfg::kVecBytes / 4));  // -lse2 pairs
+      const uint64_t* nD = nl2 + kBwdQT / 2;                                                          // -D pairs
       const int i0 = i * kBwdQT;
-      // dropout: the tile's 64 query-row hashes (thread r < 64 computes row i0 + r)
-      const uint64_t* drop_rows = reinterpret_cast<const uint64_t*>(smem_gen + Cfg::kOffDrop);
       if constexpr (DROP) {
-        named_bar_sync(3, 128);  // previous tile's hashes fully consumed
-        if (r < kBwdQT)
-          reinterpret_cast<uint64_t*>(smem_gen + Cfg::kOffDrop)[r] =
-              drop_row_hash(p.drop_seed + static_cast<uint64_t>(bh), i0 + r);
-        named_bar_sync(3, 128);
+        // the tile's 64 query-row hashes (thread r < 64 computes row i0 + r)
+        named_bar_sync(3 + sg, 128);  // previous tile's hashes fully consumed
+        if (r < kBwdQT) drop_rows[r] = drop_row_hash(p.drop_seed + static_cast<uint64_t>(bh), i0 + r);
+        named_bar_sync(3 + sg, 128);
       }
       const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0);
-      uint32_t pk[32], dk[32];
+      // masked keys: kj >= kv_limit for every query; causal: kj > i0 + c  <=>  c < kj - i0
+      const int c_lo = (kj >= sc.kv_limit) ? kBwdQT : (causal ? kj - i0 : 0);  // first visible query column
+      uint32_t sr[32], dp[32];
+      tmem_ld32_async(tX, sr);
+      tmem_ld32_async(tX + 64, dp);
+      tmem_ld_wait32(sr);
+      tmem_ld_wait32(dp);
+      const uint32_t drow = sDS + sg * Cfg::kDSBytes + r * 128;
+      auto body = [&](auto masked_t) {
+        constexpr bool kMasked = decltype(masked_t)::value;
 #pragma unroll
-      for (int c2 = 0; c2 < 32; ++c2) {
-        float pv[2], dv[2];
+        for (int half = 0; half < 2; ++half) {
+          // queries [32*half, 32*half + 32); half 1 is loaded while half 0's results are stored
+          uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = 2 * c2 + e;
-          float pr = ex2_approx(fmaf(__uint_as_float(sr[c]), sl2, -vl[c]));
-          if (need_mask) {
-            const bool masked = (kj >= sc.kv_limit) || (causal && kj > i0 + c);
-            if (masked) pr = 0.f;
+          for (int k2 = 0; k2 < 8; ++k2) {
+            const int c4 = half * 32 + 4 * k2;  // four query columns c4 .. c4 + 3
+            const ulonglong2 l4 = *reinterpret_cast<const ulonglong2*>(nl2 + (c4 >> 1));
+            const ulonglong2 d4 = *reinterpret_cast<const ulonglong2*>(nD + (c4 >> 1));
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int k = 2 * k2 + e;
+              const int c = c4 + 2 * e;
+              const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sl2x2,
+                                        e ? l4.y : l4.x);
+              float p0, p1;
+              f2_unpack(x, p0, p1);
+              p0 = ex2_approx(p0);
+              p1 = ex2_approx(p1);
+              if constexpr (kMasked) {
+                p0 = (c < c_lo) ? 0.f : p0;
+                p1 = (c + 1 < c_lo) ? 0.f : p1;
+              }
+              const uint64_t nd = e ? d4.y : d4.x;
+              if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
+                float d0, d1;
+                f2_unpack(nd, d0, d1);
+                const float z0 = drop_keep(drop_rows[c], kj, p.drop_thresh) ? p.drop_scale : 0.f;
+                const float z1 = drop_keep(drop_rows[c + 1], kj, p.drop_thresh) ? p.drop_scale : 0.f;
+                dk[k] = pack2<BF16>(p0 * fmaf(__uint_as_float(dp[2 * k]), z0, d0),
+                                    p1 * fmaf(__uint_as_float(dp[2 * k + 1]), z1, d1));
+                pk[k] = pack2<BF16>(p0 * z0, p1 * z1);
+              } else {
+                const uint64_t ds =
+                    f2_mul(f2_pack(p0, p1), f2_add(f2_pack(__uint_as_float(dp[2 * k]), __uint_as_float(dp[2 * k + 1])), nd));
+                float d0, d1;
+                f2_unpack(ds, d0, d1);
+                pk[k] = pack2<BF16>(p0, p1);
+                dk[k] = pack2<BF16>(d0, d1);
+              }
+            }
           }
-          if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
-            const float z = drop_keep(drop_rows[c], kj, p.drop_thresh) ? p.drop_scale : 0.f;
-            dv[e] = pr * (__uint_as_float(dp[c]) * z - vl[kBwdQT + c]) * tau;
-            pv[e] = pr * z;
-          } else {
-            pv[e] = pr;
-            dv[e] = pr * (__uint_as_float(dp[c]) - vl[kBwdQT + c]) * tau;
+          if (half == 0) {
+            tmem_ld32_async(tX + 32, sr);
+            tmem_ld32_async(tX + 96, dp);
+          }
+          tmem_st16(tX + half * 16, pk);       // P^T   -> X cols [0,32)
+          tmem_st16(tX + 64 + half * 16, dk);  // dS^T  -> X cols [64,96)
+          if (half == 0) {
+            // the dQ^T MMA of this warpgroup's previous tile must have released its dS^T buffer
+            mbar_wait(BAR(kBarDSEmpty + sg), dsph ^ 1);
+            dsph ^= 1;
+          }
+          // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int chunk = half * 4 + cc;
+            st_shared_v4(drow + ((chunk ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+          }
+          if (half == 0) {
+            tmem_ld_wait32(sr);
+            tmem_ld_wait32(dp);
           }
         }
-        pk[c2] = pack2<BF16>(pv[0], pv[1]);
-        dk[c2] = pack2<BF16>(dv[0], dv[1]);
-      }
-      tmem_st32(tX, pk);        // P^T   -> X_x cols [0,32)
-      tmem_st32(tX + 64, dk);   // dS^T  -> X_x cols [64,96)
-      // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
-      mbar_wait(BAR(kBarDSEmpty + (idx & 1)), dsph[idx & 1] ^ 1);
-      dsph[idx & 1] ^= 1;
-      const uint32_t drow = sDS + (idx & 1) * Cfg::kDSBytes + r * 128;
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
-        st_shared_v4(drow + ((cc ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+      };
+      if (need_mask) body(std::true_type{});
+      else body(std::false_type{});
       fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(BAR(kBarPFull + x));
-      ++idx;
+      mbar_arrive(BAR(kBarPFull + sg));
+      if (r == 0 && idx == 2) TATN_TRACE_AT(10);
     }
-    // ------------------------------------------------------------ dK / dV epilogue
-    if (idx > 0) {
+    if (r == 0 && sg == 0) TATN_TRACE_AT(3);
+    // ------------------------------------------------------------ epilogue: warpgroup 0 -> dK, 1 -> dV
+    if (n_iter > 0) {
       mbar_wait(BAR(kBarFinal), 0);
       tc_fence_after();
+      if (r == 0 && sg == 0) TATN_TRACE_AT(4);
     } else {
       mbar_wait(BAR(kBarKV), 0);  // staging reuses K/V smem
     }
+    const uint32_t tacc = tmem_base + lane_off + (sg == 0 ? Cfg::kTmemDK : Cfg::kTmemDV);
+    const uint32_t stg = sg == 0 ? sK : sV;
+    const float oscale = sg == 0 ? p.tau : 1.f;  // dK = tau * dS^T Q
+    float* grow_ptr = nullptr;
+    if constexpr (OUT_F32) {
+      grow_ptr = sg == 0 ? p.dk_f32 + static_cast<size_t>(b) * p.k_sb + static_cast<size_t>(h) * p.k_sh +
+                               static_cast<size_t>(kj) * p.k_sn
+                         : p.dv_f32 + static_cast<size_t>(b) * p.v_sb + static_cast<size_t>(h) * p.v_sh +
+                               static_cast<size_t>(kj) * p.v_sn;
+    }
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tacc = tmem_base + lane_off + (which == 0 ? Cfg::kTmemDK : Cfg::kTmemDV);
-      const uint32_t stg = which == 0 ? sK : sV;
-      float* grow_ptr = nullptr;
-      if constexpr (OUT_F32) {
-        grow_ptr = which == 0 ? p.dk_f32 + static_cast<size_t>(b) * p.k_sb + static_cast<size_t>(h) * p.k_sh +
-                                    static_cast<size_t>(kj) * p.k_sn
-                              : p.dv_f32 + static_cast<size_t>(b) * p.v_sb + static_cast<size_t>(h) * p.v_sh +
-                                    static_cast<size_t>(kj) * p.v_sn;
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      if (n_iter > 0) {
+        tmem_ld32(tacc + c * 32, v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0u;
       }
+      if constexpr (OUT_F32) {
+        if (kj < p.Nk) {
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t v[32];
-        if (idx > 0) {
-          tmem_ld32(tacc + c * 32, v);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0u;
+          for (int e = 0; e < 8; ++e)
+            reinterpret_cast<float4*>(grow_ptr + c * 32)[e] =
+                make_float4(__uint_as_float(v[4 * e]) * oscale, __uint_as_float(v[4 * e + 1]) * oscale,
+                            __uint_as_float(v[4 * e + 2]) * oscale, __uint_as_float(v[4 * e + 3]) * oscale);
         }
-        if constexpr (OUT_F32) {
-          if (kj < p.Nk) {
+      } else {
+        uint32_t pk[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              reinterpret_cast<float4*>(grow_ptr + c * 32)[e] =
-                  make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]), __uint_as_float(v[4 * e + 2]),
-                              __uint_as_float(v[4 * e + 3]));
-          }
-        } else {
-          uint32_t pk[16];
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack2<BF16>(__uint_as_float(v[2 * e]) * oscale, __uint_as_float(v[2 * e + 1]) * oscale);
+        const int sub = (c * 32) / 64;
+        const int chunk0 = ((c * 32) % 64) / 8;
+        const uint32_t rb = stg + sub * 128 * 128 + r * 128;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pk[e] = pack2<BF16>(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-          const int sub = (c * 32) / 64;
-          const int chunk0 = ((c * 32) % 64) / 8;
-          const uint32_t rb = stg + sub * 128 * 128 + r * 128;
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            st_shared_v4(rb + (((chunk0 + e) ^ (r & 7)) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
-        }
+        for (int e = 0; e < 4; ++e)
+          st_shared_v4(rb + (((chunk0 + e) ^ (r & 7)) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
       }
     }
     if constexpr (!OUT_F32) {
       fence_proxy_async_smem();
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + 4 * sg, 128);
       if (r == 0) {
-        for (int s = 0; s < Cfg::kSubs; ++s) {
-          tma_store_4d(&tmDK, sK + s * 128 * 128, s * 64, sc.k0, h, b);
-          tma_store_4d(&tmDV, sV + s * 128 * 128, s * 64, sc.k0, h, b);
-        }
+        for (int s = 0; s < Cfg::kSubs; ++s) tma_store_4d(sg == 0 ? &tmDK : &tmDV, stg + s * 128 * 128, s * 64, sc.k0, h, b);
         bulk_commit();
         bulk_wait_read_all();
       }
     }
   } else {
-    // ------------------------------------------------------------ dQ warpgroup
+    // ------------------------------------------------------------ dQ warpgroup (warps 8-11)
     const int wq = warp & 3;
     const int dd = wq * 32 + lane;  // head-dim index == TMEM lane of dQ^T
     const bool active = dd < D;
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    const float tau = p.tau;
     uint32_t fph[2] = {0, 0};
     int idx = 0;
     for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
@@ -604,39 +680,51 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(BAR(kBarDQFull + x), fph[x]);
       fph[x] ^= 1;
       tc_fence_after();
+      if (dd == 0 && idx == 2) TATN_TRACE_AT(12);
       uint32_t v[64];
       if (active) {
-        const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + x * 128;
+        const uint32_t tX = tmem_base + lane_off + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
         tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
         tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
       }
       tc_fence_before();
       mbar_arrive(BAR(kBarDQEmpty + x));
       // staging buffer free once the previous bulk reduce has read it
-      if (warp == 4 && lane == 0) bulk_wait_read_all();
+      if (warp == 8 && lane == 0) bulk_wait_read_all();
       named_bar_sync(2, 128);
       if (active) {
 #pragma unroll
         for (int c = 0; c < 64; ++c)
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sDQ + (c * D + dd) * 4), "f"(__uint_as_float(v[c])) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sDQ + (c * D + dd) * 4), "f"(__uint_as_float(v[c]) * tau)
+                       : "memory");
       }
       fence_proxy_async_smem();
       named_bar_sync(2, 128);
-      if (warp == 4 && lane == 0) {
+      if (warp == 8 && lane == 0) {
         float* dst = p.dq_acc + (static_cast<size_t>(bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D;
         asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
                      "r"(sDQ), "r"(Cfg::kDQBytes)
                      : "memory");
         bulk_commit();
+        if (idx == 2) TATN_TRACE_AT(13);
       }
       ++idx;
     }
-    if (warp == 4 && lane == 0) bulk_wait_all();
+    if (warp == 8 && lane == 0) bulk_wait_all();
+    if (warp == 8 && lane == 0) TATN_TRACE_AT(8);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (threadIdx.x == 0) {
+    TATN_TRACE_AT(7);
+#ifdef TATN_TRACE
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    if (g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 5] = smid;
+#endif
+  }
+  if (warp == kMmaWarp) {
     __syncwarp();
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
@@ -665,7 +753,7 @@ template <int D, bool BF16, bool OUT_F32, bool DROP>
 static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, const void* k, const void* v,
                                      const void* o, const void* dO, const float* lse, void* dq, void* dk, void* dv,
                                      void* ws, cudaStream_t stream, int* launches) {
-  using Cfg = tatn_dev::BwdCfg<D>;
+  using Cfg = tatn_dev::BwdCfg<D, DROP>;
   const int Nq_pad = (d.Nq + 127) / 128 * 128;
   const size_t rows = static_cast<size_t>(d.B) * d.H * Nq_pad;
   float* dq_acc = static_cast<float*>(ws);

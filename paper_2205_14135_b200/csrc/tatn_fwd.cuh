@@ -126,22 +126,6 @@ __device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, in
   return s;
 }
 
-#ifdef TATN_TRACE
-__device__ unsigned long long* g_tatn_trace = nullptr;  // [grid][8] globaltimer stamps (debug builds only)
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TATN_TRACE_AT(slot)                                                                     \
-  do {                                                                                          \
-    if (g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + (slot)] = gtimer();   \
-  } while (0)
-#else
-#define TATN_TRACE_AT(slot) \
-  do {                      \
-  } while (0)
-#endif
 
 template <int D, bool BF16, bool OUT_F32, int NQ, bool DROP>
 __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
