@@ -152,7 +152,10 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
   const int kBarSFull = kBarVEmpty + Cfg::kStages;  // + q
   const int kBarPFull = kBarSFull + 2;
   const int kBarOFinal = kBarPFull + 2;
-  const int kNumBars = kBarOFinal + 2;
+  // NQ = 1 only: S consumed into registers (QK(t+1) may overwrite it) / PV(t) complete (P free)
+  const int kBarSFree = kBarOFinal + 2;
+  const int kBarPVDone = kBarSFree + 1;
+  const int kNumBars = kBarPVDone + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffBar + 8 * 30);
 
   const int warp = static_cast<int>(warp_id());
@@ -188,6 +191,8 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
       mbar_init(BAR(kBarPFull + q), 128);
       mbar_init(BAR(kBarOFinal + q), 1);
     }
+    mbar_init(BAR(kBarSFree), 128);
+    mbar_init(BAR(kBarPVDone), 1);
     (void)kNumBars;
     fence_mbar_init();
   }
@@ -285,6 +290,53 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
       }
       __syncwarp();
     };
+    if constexpr (NQ == 1) {
+      // One Q tile: the softmax holds S(t) in registers, so QK(t+1) is issued as soon as
+      // S(t) has been read out (SFree) and runs under softmax(t); PV(t) follows P(t).
+      int t = sc.next(0);
+      int stage = 0;
+      uint32_t ph = 0, fph = 0, pph1 = 0;
+      if (t < sc.T) {
+        mbar_wait(BAR(kBarKFull + 0), 0);
+        tc_fence_after();
+        issue_qk(0, t, 0);
+        if (elect_one_sync()) mma_commit(BAR(kBarKEmpty + 0));
+        __syncwarp();
+      }
+      while (t < sc.T) {
+        const int tn = sc.next(t + 1);
+        const int sn = (stage + 1 == Cfg::kStages) ? 0 : stage + 1;
+        const uint32_t phn = (sn == 0) ? (ph ^ 1) : ph;
+        if (tn < sc.T) {
+          mbar_wait(BAR(kBarSFree), fph);
+          fph ^= 1;
+          mbar_wait(BAR(kBarKFull + sn), phn);
+          tc_fence_after();
+          issue_qk(0, tn, sn);
+          if (elect_one_sync()) mma_commit(BAR(kBarKEmpty + sn));
+          __syncwarp();
+        }
+        mbar_wait(BAR(kBarPFull + 0), pph1);
+        pph1 ^= 1;
+        mbar_wait(BAR(kBarVFull + stage), ph);
+        tc_fence_after();
+        if (elect_one_sync()) {
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk)
+            mma_ts(tmem_base + Cfg::kTmemO, tmem_base + Cfg::kTmemP + kk * 8,
+                   vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv, (acc[0] | (kk > 0 ? 1u : 0u)));
+          mma_commit(BAR(kBarPVDone));
+          mma_commit(BAR(kBarVEmpty + stage));
+        }
+        __syncwarp();
+        acc[0] = 1;
+        t = tn;
+        stage = sn;
+        ph = phn;
+      }
+      if (elect_one_sync()) mma_commit(BAR(kBarOFinal + 0));
+      __syncwarp();
+    } else {
     // Schedule per K/V tile t (union order over the CTA's two Q tiles):
     //   PV_A(t), QK_A(t+1), PV_B(t), QK_B(t+1)
     // so softmax A(t+1) starts while softmax B(t) still runs (ping-pong). The
@@ -369,6 +421,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     if (elect_one_sync())
       for (int q = 0; q < NQ; ++q) mma_commit(BAR(kBarOFinal + q));
     __syncwarp();
+    }  // NQ == 2
   }
   } else {
     if constexpr (NQ == 2) setmaxnreg_inc<208>();  // 2*128*(208-168) <= 128*(168-80)
@@ -393,12 +446,133 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     if constexpr (DROP) drow = drop_row_hash(p.drop_seed + static_cast<uint64_t>(bh), grow);
     const float sl2 = p.scale_log2;
     const bool causal = p.mask_kind == kMaskCausal;
+    const uint64_t sl2x2 = f2_pack(sl2, sl2);
 
     float m_run = -INFINITY;  // running max of tau*s*log2(e), possibly stale by <= threshold
     float l_run = 0.f;        // running denominator relative to m_run
     int n_done = 0;
     uint32_t sph = 0;
 
+    if constexpr (NQ == 1) {
+      // One Q tile per CTA (d = 64, two CTAs per SM). S(t) is pulled into registers at
+      // once and released (SFree) so QK(t+1) runs under this tile's exponentials; P(t)
+      // goes to its own TMEM columns once PV(t-1) has drained them (PVDone).
+      uint32_t pvph = 0;
+      auto wait_pv = [&]() {
+        mbar_wait(BAR(kBarPVDone), pvph);
+        pvph ^= 1;
+        tc_fence_after();
+      };
+      for (int t = sc.next(0); t < sc.T; t = sc.next(t + 1)) {
+        mbar_wait(BAR(kBarSFull + 0), sph);
+        sph ^= 1;
+        tc_fence_after();
+        if (threadIdx.x == 0 && n_done == 0) TATN_TRACE_AT(1);
+        if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(8);
+        if (threadIdx.x == 0 && n_done == 3) TATN_TRACE_AT(13);
+        uint32_t sv[4][32];
+        tmem_ld32_async(tS, sv[0]);
+        tmem_ld32_async(tS + 32, sv[1]);
+        tmem_ld32_async(tS + 64, sv[2]);
+        tmem_ld32_async(tS + 96, sv[3]);
+        tmem_ld_wait32(sv[0]);
+        tmem_ld_wait32(sv[1]);
+        tmem_ld_wait32(sv[2]);
+        tmem_ld_wait32(sv[3]);
+        tc_fence_before();
+        mbar_arrive(BAR(kBarSFree));
+        const int k0 = t * kBN;
+        const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0);
+        const int lim = min(sc.kv_limit, causal ? grow + 1 : sc.kv_limit) - k0;  // columns >= lim are masked
+        auto step = [&](auto masked_t) {
+          constexpr bool kMasked = decltype(masked_t)::value;
+          if constexpr (kMasked) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                sv[c][i] = (c * 32 + i >= lim) ? __float_as_uint(-INFINITY) : sv[c][i];
+          }
+          float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              mx0 = fmax3(mx0, __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
+              mx1 = fmax3(mx1, __uint_as_float(sv[c][i + 2]), __uint_as_float(sv[c][i + 3]));
+            }
+          const float m_tile = fmaxf(mx0, mx1) * sl2;
+          const bool jump = m_tile - m_run > kRescaleThreshold;  // false when both are -inf
+          bool pv_ready = n_done == 0;
+          if (__any_sync(0xffffffffu, jump)) {  // warp-uniform: TMEM ld/st below are .sync.aligned
+            float alpha = 1.f;
+            if (jump) {
+              alpha = ex2_approx(m_run - m_tile);  // 0 when m_run == -inf
+              m_run = m_tile;
+              l_run *= alpha;
+            }
+            if (!pv_ready) {
+              wait_pv();  // O is final up to tile t-1
+              pv_ready = true;
+#pragma unroll 1
+              for (int c = 0; c < D / 16; ++c) {  // 16 columns at a time: S(t) is still live
+                uint32_t o[16];
+                tmem_ld16(tO + c * 16, o);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                tmem_st16(tO + c * 16, o);
+              }
+            }
+          }
+          const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+          const uint64_t negm = f2_pack(-m_use, -m_use);
+          uint64_t rsum0 = f2_pack(0.f, 0.f), rsum1 = rsum0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int i = c * 16 + k;
+              const uint64_t x =
+                  f2_fma(f2_pack(__uint_as_float(sv[c][2 * k]), __uint_as_float(sv[c][2 * k + 1])), sl2x2, negm);
+              uint64_t pv;
+              // the polynomial needs finite x: full tiles only (m_run <= true max + threshold)
+              if (!kMasked && !DROP && kEmuPairs > 0 && (i & 7) < kEmuPairs) {
+                pv = exp2_poly_f2(x);
+              } else {
+                float x0, x1;
+                f2_unpack(x, x0, x1);
+                pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
+              }
+              float p0, p1;
+              f2_unpack(pv, p0, p1);
+              if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
+                const int j0 = k0 + c * 32 + 2 * k;
+                p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
+                p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
+              }
+              pk[k] = pack2<BF16>(p0, p1);
+              if (k & 1) rsum1 = f2_add(rsum1, pv);
+              else rsum0 = f2_add(rsum0, pv);
+            }
+            if (c == 0 && !pv_ready) wait_pv();  // PV(t-1) has read P(t-1)
+            tmem_st16(tP + c * 16, pk);
+          }
+          float rs0, rs1, rs2, rs3;
+          f2_unpack(rsum0, rs0, rs1);
+          f2_unpack(rsum1, rs2, rs3);
+          l_run += (rs0 + rs1) + (rs2 + rs3);
+        };
+        if (need_mask) step(std::true_type{});
+        else step(std::false_type{});
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(BAR(kBarPFull + 0));
+        if (threadIdx.x == 0) TATN_TRACE_AT(2);
+        if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(10);
+        ++n_done;
+      }
+    } else {
     for (int t = sc.next(0); t < sc.T; t = sc.next(t + 1)) {
       if (!is_member(t)) continue;
       mbar_wait(BAR(kBarSFull + q), sph);
@@ -419,7 +593,6 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
           }
         }
       };
-      const uint64_t sl2x2 = f2_pack(sl2, sl2);
       // One streaming pass over S: p = 2^(s*scale_log2 - m_use) per 32-column chunk
       // (FFMA2 scale, MUFU ex2 or the FMA-pipe polynomial for (i & 7) < kEmuPairs on
       // full tiles), P (16-bit) to TMEM at tP, row sum in FP32x2; optionally tracks
@@ -570,6 +743,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
       if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(10);
       ++n_done;
     }
+    }  // NQ == 2
 
     n_steps_dbg = n_done;
     // ------------------------------------------------------------ epilogue

@@ -11,4 +11,4 @@ print("value", d["value"], "ms", d["ms_per_step"], {k: (v["avg_launch_ms"], v["t
 for s in d.get("sweep", []):
     print(f'{s["workload"]:>14} fwd {s["fwd_tflops"]:7.1f} bwd {s["bwd_tflops"]:7.1f}')
 PY
-[ -f paper_2205_14135_b200/lib/variants/lib_trace.so ] && timeout 120 python scripts/trace_bwd.py 2>&1 | grep -v Warn
+[ -f paper_2205_14135_b200/lib/variants/lib_trace.so ] && timeout 120 python scripts/trace_${TRACE:-bwd}.py 2>&1 | grep -v Warn
