@@ -93,7 +93,7 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
              float* lse, void* stream);
 
 /* Workspace for tatn_bwd: fp32 dQ accumulator [B,H,Nq_pad,d] + lse2 and D vectors
- * [B,H,Nq_pad], Nq_pad = Nq rounded up to 128. */
+ * [B,H,Nq_pad], Nq_pad = Nq rounded up to 128, + 16 bytes (persistent scheduler counter). */
 size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc);
 
 /* Backward with recomputation from lse (Algorithm 4).

@@ -53,18 +53,21 @@ struct BwdCfg {
   static constexpr int kDSBytes = 128 * 128;          // 128 keys x 64 q x 2B
   static constexpr int kDQBytes = kBwdQT * D * 4;     // fp32 staging
   static constexpr int kVecBytes = 2 * kBwdQT * 4;    // lse2 + D
-  static constexpr int kOffK = 0;
-  static constexpr int kOffV = kOffK + kKVTile;
-  static constexpr int kOffQ = kOffV + kKVTile;
+  // K/V buffers: double-buffered at d = 64 (the next item's K/V lands while this one runs)
+  static constexpr int kKVBufs = (D == 64) ? 2 : 1;
+  static constexpr int kOffKV = 0;
+  static constexpr int kOffQ = kOffKV + kKVBufs * 2 * kKVTile;
   static constexpr int kOffDO = kOffQ + kStages * kQTile;
   static constexpr int kOffDS = kOffDO + kStages * kQTile;
   static constexpr int kOffDQ = kOffDS + 2 * kDSBytes;
   static constexpr int kOffVec = kOffDQ + kDQBytes;
   static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
-  static constexpr int kOffMask = kOffBar + 256;       // block-sparse q-tile bitmask, 128 words
+  static constexpr int kOffRing = kOffBar + 384;       // item ring (kItemRing ints)
+  static constexpr int kOffMask = kOffRing + 64;       // block-sparse q-tile bitmask, 128 words
   static constexpr int kOffDrop = kOffMask + 512;      // dropout: 64 query-row hashes per softmax warpgroup
   static constexpr int kSmemBytes = kOffDrop + (DROP ? 1024 : 0);  // dynamic smem is declared __align__(1024)
   static_assert(kSmemBytes <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
+  static_assert(2 * 128 * D * 2 <= kOffVec - kOffDS, "dK/dV staging must fit the dS^T + dQ staging region");
   static constexpr uint32_t kTmemX = 0;    // X_x = x*128: S^T [0,64) dP^T [64,128)
   static constexpr uint32_t kTmemDV = 256;
   static constexpr uint32_t kTmemDK = 256 + D;
@@ -133,12 +136,14 @@ template <int D, bool BF16, bool O_F32>
 __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_, const uint16_t* __restrict__ dO,
                                                     const float* __restrict__ lse, int64_t ob, int64_t oh, int64_t on,
                                                     int B, int H, int Nq, int Nq_pad, float* __restrict__ lse2,
-                                                    float* __restrict__ delta, float* __restrict__ dq_acc) {
+                                                    float* __restrict__ delta, float* __restrict__ dq_acc,
+                                                    int* __restrict__ item_counter) {
   constexpr int kChunks = D / 8;
   const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long row = gid / kChunks;  // over B*H*Nq_pad
   const int c = static_cast<int>(gid % kChunks);
   const long long total = static_cast<long long>(B) * H * Nq_pad;
+  if (gid == 0) *item_counter = 0;  // K3's persistent scheduler starts from item 0
   float part = 0.f;
   int qi = 0;
   long long bh = 0;
@@ -226,6 +231,20 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
 }
 
 // ---------------------------------------------------------------- K3
+// Item w (one 128-key tile of one head) -> (bh, j). Items are laid out in head groups:
+// the key tiles of `group` heads are adjacent, so their Q / dO tiles and fp32 dQ
+// accumulators stay L2-resident; within a group the heaviest tiles (j = 0 under a
+// causal mask) come first.
+__device__ __forceinline__ void bwd_item(const BwdParams& p, int w, int& bh, int& j) {
+  const int per_group = p.group * p.n_ktiles;
+  const int grp = w / per_group;
+  const int r = w - grp * per_group;
+  const int gsz = min(p.group, p.B * p.H - grp * p.group);
+  j = r / gsz;
+  bh = grp * p.group + (r - j * gsz);
+}
+constexpr int kItemRing = 4;  // items published by the producer warp to the other roles
+
 template <int D, bool BF16, bool OUT_F32, bool DROP>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     tatn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -234,79 +253,80 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     const BwdParams p, const float* __restrict__ lse2, int Nq_pad) {
   using Cfg = BwdCfg<D, DROP>;
   constexpr int S = Cfg::kStages;
+  constexpr int NKV = Cfg::kKVBufs;
   constexpr int kProducerWarp = 12, kMmaWarp = 13;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // 128B-swizzle atoms need 1024B alignment
   const uint32_t smem_base = smem_u32(smem_raw);
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
 
-  const uint32_t sK = smem_base + Cfg::kOffK;
-  const uint32_t sV = smem_base + Cfg::kOffV;
+  const uint32_t sKV = smem_base + Cfg::kOffKV;  // buffer b: K at b*2*kKVTile, V at +kKVTile
   const uint32_t sQ = smem_base + Cfg::kOffQ;
   const uint32_t sDO = smem_base + Cfg::kOffDO;
   const uint32_t sDS = smem_base + Cfg::kOffDS;
   const uint32_t sDQ = smem_base + Cfg::kOffDQ;
+  const uint32_t sStage = sDS;  // dK / dV output staging reuses the dS^T + dQ staging region
   const uint32_t sVec = smem_base + Cfg::kOffVec;
   const float* vec_gen = reinterpret_cast<const float*>(smem_gen + Cfg::kOffVec);
   const uint32_t bar0 = smem_base + Cfg::kOffBar;
   auto BAR = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
-  const int kBarKV = 0;
-  const int kBarQFull = 1;
+  const int kBarQFull = 0;
   const int kBarQEmpty = kBarQFull + S;
-  const int kBarSFull = kBarQEmpty + S;   // [2]
-  const int kBarPFull = kBarSFull + 2;    // [2]
-  const int kBarDQFull = kBarPFull + 2;   // [2]
-  const int kBarDQEmpty = kBarDQFull + 2; // [2]
-  const int kBarDSEmpty = kBarDQEmpty + 2;// [2]
-  const int kBarFinal = kBarDSEmpty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffBar + 8 * 28);
+  const int kBarSFull = kBarQEmpty + S;     // [2]
+  const int kBarPFull = kBarSFull + 2;      // [2]
+  const int kBarDQFull = kBarPFull + 2;     // [2]
+  const int kBarDQEmpty = kBarDQFull + 2;   // [2]
+  const int kBarDSEmpty = kBarDQEmpty + 2;  // [2]
+  const int kBarKVFull = kBarDSEmpty + 2;   // [NKV]
+  const int kBarKVFree = kBarKVFull + NKV;  // [NKV] MMAs of the buffer's item done
+  const int kBarFinal = kBarKVFree + NKV;   // item's MMAs done (dK, dV final in TMEM)
+  const int kBarAccFree = kBarFinal + 1;    // dK / dV drained from TMEM (count 128)
+  const int kBarStageFree = kBarAccFree + 1;// output staging read by the TMA store
+  const int kBarItem = kBarStageFree + 1;   // [kItemRing] item id published
+  const int kBarItemFree = kBarItem + kItemRing;  // [kItemRing] slot read by all 13 consumer warps
+  const int kNumBars = kBarItemFree + kItemRing;
+  static_assert(8 * (2 * S + 10 + 2 * NKV + 3 + 2 * kItemRing) <= 8 * 46, "barrier region");
+  volatile int* ring = reinterpret_cast<volatile int*>(smem_gen + Cfg::kOffRing);
+  // Dense launches are persistent (one CTA per SM): the producer claims items from a
+  // global counter (zeroed by K2) and publishes them; block-sparse launches run exactly
+  // one item per CTA (item = blockIdx.x).
+  auto take_item = [&](int n) -> int {  // called by whole warps
+    mbar_wait(BAR(kBarItem + n % kItemRing), static_cast<uint32_t>((n / kItemRing) & 1));
+    const int w = ring[n % kItemRing];
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(BAR(kBarItemFree + n % kItemRing));
+    return w;
+  };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffBar + 8 * 46);
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
-  // 1-D grid in head groups: the key tiles of `group` heads run together, so their
-  // Q / dO tiles and fp32 dQ accumulators stay L2-resident; within a group the
-  // heaviest tiles (j = 0 under a causal mask) are dispatched first.
-  int bh, j;
-  {
-    const int per_group = p.group * p.n_ktiles;
-    const int grp = static_cast<int>(blockIdx.x) / per_group;
-    const int r = static_cast<int>(blockIdx.x) - grp * per_group;
-    const int gsz = min(p.group, p.B * p.H - grp * p.group);
-    j = r / gsz;
-    bh = grp * p.group + (r - j * gsz);
-  }
-  const int b = bh / p.H;
-  const int h = bh - b * p.H;
   uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
   if (threadIdx.x == 0) TATN_TRACE_AT(0);
 
   if (threadIdx.x == 0) {
-    mbar_init(BAR(kBarKV), 1);
-    for (int s = 0; s < S; ++s) {
-      mbar_init(BAR(kBarQFull + s), 1);
-      mbar_init(BAR(kBarQEmpty + s), 1);
-    }
+    for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
     for (int x = 0; x < 2; ++x) {
-      mbar_init(BAR(kBarSFull + x), 1);
       mbar_init(BAR(kBarPFull + x), 128);
-      mbar_init(BAR(kBarDQFull + x), 1);
       mbar_init(BAR(kBarDQEmpty + x), 128);
-      mbar_init(BAR(kBarDSEmpty + x), 1);
     }
-    mbar_init(BAR(kBarFinal), 1);
+    mbar_init(BAR(kBarAccFree), 128);
+    for (int k = 0; k < kItemRing; ++k) mbar_init(BAR(kBarItemFree + k), 13);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
     tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_relinquish();
   }
-  BwdSched sc = make_bwd_sched(p, b, j);
-  sc.mask = mask_smem;
-  if (sc.gcol != nullptr && warp == kProducerWarp) {
-    // block-sparse: read grid column j once into a bitmask over 64-row Q tiles
+  // block-sparse launches run one item per CTA (grid = items): its grid column is read once
+  // into a bitmask over 64-row Q tiles
+  if (p.grid != nullptr && warp == kProducerWarp) {
+    int bh0, j0;
+    bwd_item(p, static_cast<int>(blockIdx.x), bh0, j0);
+    const uint8_t* gcol = p.grid + j0;
     for (int base = 0; base < p.tr; base += 32) {
       const int r = base + lane;
-      const bool v = r < p.tr && sc.gcol[static_cast<size_t>(r) * p.tc] != 0;
+      const bool v = r < p.tr && gcol[static_cast<size_t>(r) * p.tc] != 0;
       const uint32_t bits = __ballot_sync(0xffffffffu, v);
       if (lane == 0) {
         mask_smem[(2 * base) >> 5] = spread_bits16(bits);
@@ -318,9 +338,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // number of Q tiles this key tile visits (same order for every role)
-  int n_iter = 0;
-  for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) ++n_iter;
+
+  // per-item schedule, identical in every role
+  struct Item {
+    int bh, b, h, j, cnt;
+    BwdSched sc;
+  };
+  auto item = [&](int w) {
+    Item it;
+    bwd_item(p, w, it.bh, it.j);
+    it.b = it.bh / p.H;
+    it.h = it.bh - it.b * p.H;
+    it.sc = make_bwd_sched(p, it.b, it.j);
+    it.sc.mask = mask_smem;
+    it.cnt = 0;
+    if (it.sc.gcol == nullptr) it.cnt = it.sc.i_end - it.sc.i_begin;
+    else
+      for (int i = it.sc.next(it.sc.i_begin); i < it.sc.i_end; i = it.sc.next(i + 1)) ++it.cnt;
+    return it;
+  };
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -330,39 +366,62 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmDO);
-      mbar_expect_tx(BAR(kBarKV), 2 * Cfg::kKVTile);
-      for (int s = 0; s < Cfg::kSubs; ++s) {
-        tma_load_4d(sK + s * 128 * 128, &tmK, BAR(kBarKV), s * 64, sc.k0, h, b);
-        tma_load_4d(sV + s * 128 * 128, &tmV, BAR(kBarKV), s * 64, sc.k0, h, b);
-      }
     }
     __syncwarp();
-    int stage = 0;
-    uint32_t ph = 0;
-    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
-      mbar_wait(BAR(kBarQEmpty + stage), ph ^ 1);
-      if (elect_one_sync()) {
-        const uint32_t fb = BAR(kBarQFull + stage);
-        mbar_expect_tx(fb, 2 * Cfg::kQTile + Cfg::kVecBytes);
-        for (int s = 0; s < Cfg::kSubs; ++s) {
-          tma_load_4d(sQ + stage * Cfg::kQTile + s * Cfg::kQSub, &tmQ, fb, s * 64, i * kBwdQT, h, b);
-          tma_load_4d(sDO + stage * Cfg::kQTile + s * Cfg::kQSub, &tmDO, fb, s * 64, i * kBwdQT, h, b);
-        }
-        const float* src = lse2 + static_cast<size_t>(bh) * Nq_pad + i * kBwdQT;
-        const uint32_t vdst = sVec + stage * Cfg::kVecBytes;
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(vdst),
-                     "l"(src), "r"(kBwdQT * 4), "r"(fb)
-                     : "memory");
-        const float* srcd = p.delta + static_cast<size_t>(bh) * Nq_pad + i * kBwdQT;
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         vdst + kBwdQT * 4),
-                     "l"(srcd), "r"(kBwdQT * 4), "r"(fb)
-                     : "memory");
+    int g = 0;  // Q tiles loaded so far (ring position)
+    for (int n = 0;; ++n) {
+      // claim item n of this CTA and publish it in ring slot n % kItemRing
+      if (n >= kItemRing)
+        mbar_wait(BAR(kBarItemFree + n % kItemRing), static_cast<uint32_t>((n / kItemRing - 1) & 1));
+      int w = -1;
+      if (p.grid != nullptr) {
+        w = (n == 0) ? static_cast<int>(blockIdx.x) : -1;
+      } else if (lane == 0) {
+        w = atomicAdd(p.item_counter, 1);
+      }
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (w >= p.n_items) w = -1;
+      if (lane == 0) {
+        ring[n % kItemRing] = w;
+        mbar_arrive(BAR(kBarItem + n % kItemRing));
       }
       __syncwarp();
-      if (++stage == S) {
-        stage = 0;
-        ph ^= 1;
+      if (w < 0) break;
+      const Item it = item(w);
+      const int kb = n % NKV;
+      if (n >= NKV) mbar_wait(BAR(kBarKVFree + kb), static_cast<uint32_t>((n / NKV - 1) & 1));
+      if (elect_one_sync()) {
+        const uint32_t sK = sKV + kb * 2 * Cfg::kKVTile, sV = sK + Cfg::kKVTile;
+        mbar_expect_tx(BAR(kBarKVFull + kb), 2 * Cfg::kKVTile);
+        for (int s = 0; s < Cfg::kSubs; ++s) {
+          tma_load_4d(sK + s * 128 * 128, &tmK, BAR(kBarKVFull + kb), s * 64, it.sc.k0, it.h, it.b);
+          tma_load_4d(sV + s * 128 * 128, &tmV, BAR(kBarKVFull + kb), s * 64, it.sc.k0, it.h, it.b);
+        }
+      }
+      __syncwarp();
+      for (int i = it.sc.next(it.sc.i_begin); i < it.sc.i_end; i = it.sc.next(i + 1), ++g) {
+        const int stage = g % S;
+        mbar_wait(BAR(kBarQEmpty + stage), static_cast<uint32_t>(((g / S) & 1) ^ 1));
+        if (elect_one_sync()) {
+          const uint32_t fb = BAR(kBarQFull + stage);
+          mbar_expect_tx(fb, 2 * Cfg::kQTile + Cfg::kVecBytes);
+          for (int s = 0; s < Cfg::kSubs; ++s) {
+            tma_load_4d(sQ + stage * Cfg::kQTile + s * Cfg::kQSub, &tmQ, fb, s * 64, i * kBwdQT, it.h, it.b);
+            tma_load_4d(sDO + stage * Cfg::kQTile + s * Cfg::kQSub, &tmDO, fb, s * 64, i * kBwdQT, it.h, it.b);
+          }
+          const float* src = lse2 + static_cast<size_t>(it.bh) * Nq_pad + i * kBwdQT;
+          const uint32_t vdst = sVec + stage * Cfg::kVecBytes;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           vdst),
+                       "l"(src), "r"(kBwdQT * 4), "r"(fb)
+                       : "memory");
+          const float* srcd = p.delta + static_cast<size_t>(it.bh) * Nq_pad + i * kBwdQT;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           vdst + kBwdQT * 4),
+                       "l"(srcd), "r"(kBwdQT * 4), "r"(fb)
+                       : "memory");
+        }
+        __syncwarp();
       }
     }
   } else if (warp == kMmaWarp) {
@@ -373,345 +432,376 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     constexpr uint32_t idesc_acc = make_idesc_f16(ab, 128, D, 0, 1);      // dV, dK (B MN-major)
     constexpr uint32_t idesc_dq = make_idesc_f16(ab, 128, kBwdQT, 1, 1);  // dQ^T (A, B MN-major)
     // base descriptors; per-MMA operands add (byte offset >> 4) to the start-address field
-    const uint64_t dK0 = make_sdesc_sw128(sK, 16, 1024);                 // K as K-major A
-    const uint64_t dV0 = make_sdesc_sw128(sV, 16, 1024);                 // V as K-major A
+    const uint64_t dKV0 = make_sdesc_sw128(sKV, 16, 1024);               // K / V as K-major A
     const uint64_t dQk0 = make_sdesc_sw128(sQ, 16, 1024);                // Q as K-major B
     const uint64_t dDOk0 = make_sdesc_sw128(sDO, 16, 1024);              // dO as K-major B
     const uint64_t dQmn0 = make_sdesc_sw128(sQ, Cfg::kQSub, 1024);       // Q as MN-major B
     const uint64_t dDOmn0 = make_sdesc_sw128(sDO, Cfg::kQSub, 1024);     // dO as MN-major B
-    const uint64_t dKmn0 = make_sdesc_sw128(sK, 128 * 128, 1024);        // K^T as MN-major A
+    const uint64_t dKmn0 = make_sdesc_sw128(sKV, 128 * 128, 1024);       // K^T as MN-major A
     const uint64_t dDS0 = make_sdesc_sw128(sDS, 128 * 128, 1024);        // dS^T as MN-major B
-    const int n = n_iter;
-    mbar_wait(BAR(kBarKV), 0);
-    tc_fence_after();
-    if (lane == 0) TATN_TRACE_AT(1);
+    int g0 = 0;  // Q tiles issued before the current item
+    for (int n = 0;; ++n) {
+      const int w = take_item(n);
+      if (w < 0) break;
+      const int cnt = item(w).cnt;
+      const int kb = n % NKV;
+      const uint32_t koff = static_cast<uint32_t>(kb * 2 * Cfg::kKVTile);  // K of buffer kb
+      const uint32_t voff = koff + Cfg::kKVTile;
+      mbar_wait(BAR(kBarKVFull + kb), static_cast<uint32_t>((n / NKV) & 1));
+      tc_fence_after();
+      if (lane == 0 && n == 0) TATN_TRACE_AT(1);
 #ifdef TATN_TRACE
-    if (lane == 0 && g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 6] = n;
+      if (lane == 0 && n == 0 && g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 6] = cnt;
 #endif
-    uint32_t qph = 0;  // phase bit per Q/dO stage (bit s)
-    uint32_t pph = 0, eph = 0;  // phase bits per X buffer (bit x)
-
-    auto front_dp = [&](int idx) {
-      const int s = idx % S;
-      const int x = idx & 1;
-      mbar_wait(BAR(kBarQFull + s), (qph >> s) & 1u);
-      qph ^= 1u << s;
-      tc_fence_after();
-      if (elect_one_sync()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t offa = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
-          mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, dV0 + (offa >> 4),
-                 dDOk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
-        }
-      }
-      __syncwarp();
-    };
-    auto front_s = [&](int idx) {
-      const int s = idx % S;
-      const int x = idx & 1;
-      if (elect_one_sync()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t offa = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
-          mma_ss(tmem_base + Cfg::kTmemX + x * 128, dK0 + (offa >> 4), dQk0 + ((s * Cfg::kQTile + offb) >> 4),
-                 idesc_s, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(BAR(kBarSFull + x));
-      }
-      __syncwarp();
-    };
-
-    for (int idx = 0; idx < n && idx < 2; ++idx) {
-      front_dp(idx);
-      front_s(idx);
-    }
-    for (int idx = 0; idx < n; ++idx) {
-      const int x = idx & 1;
-      const int s = idx % S;
-      mbar_wait(BAR(kBarPFull + x), (pph >> x) & 1u);
-      pph ^= 1u << x;
-      tc_fence_after();
-      if (lane == 0 && idx == 2) TATN_TRACE_AT(11);
-      const uint32_t accf = idx > 0 ? 1u : 0u;
-      if (elect_one_sync()) {
-        // dV += P^T dO   (P^T bf16 in X_x cols [0,32); dO MN-major, 16 queries per step)
-#pragma unroll
-        for (int kk = 0; kk < kBwdQT / 16; ++kk)
-          mma_ts(tmem_base + Cfg::kTmemDV, tmem_base + Cfg::kTmemX + x * 128 + kk * 8,
-                 dDOmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc, accf | (kk > 0 ? 1u : 0u));
-        // dK += dS^T Q   (dS^T bf16 in X_x cols [64,96))
-#pragma unroll
-        for (int kk = 0; kk < kBwdQT / 16; ++kk)
-          mma_ts(tmem_base + Cfg::kTmemDK, tmem_base + Cfg::kTmemX + x * 128 + 64 + kk * 8,
-                 dQmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc, accf | (kk > 0 ? 1u : 0u));
-      }
-      __syncwarp();
-      auto issue_dq = [&]() {
-        // dQ^T = K^T dS^T  (K MN-major as A; dS^T MN-major as B; 16 keys per step)
-        const uint32_t tDQ = tmem_base + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
+      auto front_dp = [&](int g) {  // dP^T = V dO^T  -> X cols [64,128)
+        const int s = g % S;
+        const int x = g & 1;
+        mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>((g / S) & 1));
+        tc_fence_after();
         if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < kBwdKT / 16; ++kk)
-            mma_ss(tDQ, dKmn0 + ((kk * 2048) >> 4), dDS0 + ((x * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq,
-                   kk > 0 ? 1u : 0u);
-          mma_commit(BAR(kBarDQFull + x));
-          mma_commit(BAR(kBarQEmpty + s));
-          mma_commit(BAR(kBarDSEmpty + x));
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t offa = voff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+            const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+            mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, dKV0 + (offa >> 4),
+                   dDOk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
+          }
         }
         __syncwarp();
       };
-      if constexpr (Cfg::kSepDQ) {
-        // X_x is free once dV/dK have read P^T / dS^T (in-order pipe): start the next front
-        // first so S^T(idx + 2) reaches the softmax warpgroup one dQ^T earlier
-        if (idx + 2 < n) {
-          front_dp(idx + 2);
-          front_s(idx + 2);
+      auto front_s = [&](int g) {  // S^T = K Q^T  -> X cols [0,64)
+        const int s = g % S;
+        const int x = g & 1;
+        if (elect_one_sync()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t offa = koff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+            const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+            mma_ss(tmem_base + Cfg::kTmemX + x * 128, dKV0 + (offa >> 4), dQk0 + ((s * Cfg::kQTile + offb) >> 4),
+                   idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(BAR(kBarSFull + x));
         }
-        if (idx >= 2) {
-          mbar_wait(BAR(kBarDQEmpty + x), (eph >> x) & 1u);  // dQ^T(idx - 2) drained from buffer x
-          eph ^= 1u << x;
+        __syncwarp();
+      };
+      auto wait_dq_drained = [&](int g) {  // dQ^T of Q tile g read out of its TMEM buffer
+        mbar_wait(BAR(kBarDQEmpty + (g & 1)), static_cast<uint32_t>((g >> 1) & 1));
+        tc_fence_after();
+      };
+      for (int i = 0; i < cnt && i < 2; ++i) {
+        const int g = g0 + i;
+        front_dp(g);
+        if (!Cfg::kSepDQ && g >= 2) wait_dq_drained(g - 2);  // X_x still holds dQ^T(g - 2)
+        front_s(g);
+      }
+      for (int i = 0; i < cnt; ++i) {
+        const int g = g0 + i;
+        const int x = g & 1;
+        const int s = g % S;
+        mbar_wait(BAR(kBarPFull + x), static_cast<uint32_t>((g >> 1) & 1));
+        tc_fence_after();
+        if (i == 0 && n > 0) {
+          mbar_wait(BAR(kBarAccFree), static_cast<uint32_t>((n - 1) & 1));  // previous dK / dV drained
           tc_fence_after();
         }
-        issue_dq();
-      } else {
-        issue_dq();  // dQ^T lands in X_x cols [0,64): the next front waits for the dQ warpgroup
-        if (idx + 2 < n) {
-          front_dp(idx + 2);
-          mbar_wait(BAR(kBarDQEmpty + x), (eph >> x) & 1u);
-          eph ^= 1u << x;
-          tc_fence_after();
-          front_s(idx + 2);
+        if (lane == 0 && i == 2 && n == 0) TATN_TRACE_AT(11);
+        const uint32_t accf = i > 0 ? 1u : 0u;
+        if (elect_one_sync()) {
+          // dV += P^T dO   (P^T 16-bit in X_x cols [0,32); dO MN-major, 16 queries per step)
+#pragma unroll
+          for (int kk = 0; kk < kBwdQT / 16; ++kk)
+            mma_ts(tmem_base + Cfg::kTmemDV, tmem_base + Cfg::kTmemX + x * 128 + kk * 8,
+                   dDOmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc, accf | (kk > 0 ? 1u : 0u));
+          // dK += dS^T Q   (dS^T 16-bit in X_x cols [64,96))
+#pragma unroll
+          for (int kk = 0; kk < kBwdQT / 16; ++kk)
+            mma_ts(tmem_base + Cfg::kTmemDK, tmem_base + Cfg::kTmemX + x * 128 + 64 + kk * 8,
+                   dQmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc, accf | (kk > 0 ? 1u : 0u));
+        }
+        __syncwarp();
+        auto issue_dq = [&]() {
+          // dQ^T = K^T dS^T  (K MN-major as A; dS^T MN-major as B; 16 keys per step)
+          const uint32_t tDQ = tmem_base + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
+          if (elect_one_sync()) {
+#pragma unroll
+            for (int kk = 0; kk < kBwdKT / 16; ++kk)
+              mma_ss(tDQ, dKmn0 + ((koff + kk * 2048) >> 4), dDS0 + ((x * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq,
+                     kk > 0 ? 1u : 0u);
+            mma_commit(BAR(kBarDQFull + x));
+            mma_commit(BAR(kBarQEmpty + s));
+            mma_commit(BAR(kBarDSEmpty + x));
+          }
+          __syncwarp();
+        };
+        if constexpr (Cfg::kSepDQ) {
+          // X_x is free once dV/dK have read P^T / dS^T (in-order pipe): start the next front
+          // first so S^T(g + 2) reaches the softmax warpgroup one dQ^T earlier
+          if (i + 2 < cnt) {
+            front_dp(g + 2);
+            front_s(g + 2);
+          }
+          if (g >= 2) wait_dq_drained(g - 2);  // dQ^T buffer x free
+          issue_dq();
+        } else {
+          issue_dq();  // dQ^T lands in X_x cols [0,64): the next front waits for the dQ warpgroup
+          if (i + 2 < cnt) {
+            front_dp(g + 2);
+            wait_dq_drained(g);
+            front_s(g + 2);
+          }
         }
       }
+      if (elect_one_sync()) {
+        mma_commit(BAR(kBarFinal));
+        mma_commit(BAR(kBarKVFree + kb));
+      }
+      __syncwarp();
+      g0 += cnt;
     }
-    if (elect_one_sync()) mma_commit(BAR(kBarFinal));
-    __syncwarp();
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax warpgroups
     const int sg = warp >> 2;               // warpgroup = X buffer = parity of its Q tiles
     const int r = (warp & 3) * 32 + lane;   // key row within tile == TMEM lane
-    const int kj = sc.k0 + r;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const float sl2 = p.scale_log2;
     const uint64_t sl2x2 = f2_pack(sl2, sl2);
     const bool causal = p.mask_kind == kMaskCausal;
-    uint32_t sph = 0, dsph = 0;
     const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + sg * 128;
     uint64_t* drop_rows = reinterpret_cast<uint64_t*>(smem_gen + Cfg::kOffDrop + sg * 512);
-    int idx = 0;
-    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1), ++idx) {
-      if ((idx & 1) != sg) continue;
-      const int s = idx % S;
-      if (p.visited != nullptr && r == 0) {
-        const long long bit = static_cast<long long>(i >> 1) * p.tc + j;
-        atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
-      }
-      mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>(idx / S) & 1u);  // lse2 / D vectors landed
-      mbar_wait(BAR(kBarSFull + sg), sph);
-      sph ^= 1;
-      tc_fence_after();
-      if (r == 0 && idx == 0) TATN_TRACE_AT(2);
-      if (r == 0 && idx == 2) TATN_TRACE_AT(9);
-      const uint64_t* nl2 = reinterpret_cast<const uint64_t*>(vec_gen + s * (Cfg::kVecBytes / 4));  // -lse2 pairs
-      const uint64_t* nD = nl2 + kBwdQT / 2;                                                          // -D pairs
-      const int i0 = i * kBwdQT;
-      if constexpr (DROP) {
-        // the tile's 64 query-row hashes (thread r < 64 computes row i0 + r)
-        named_bar_sync(3 + sg, 128);  // previous tile's hashes fully consumed
-        if (r < kBwdQT) drop_rows[r] = drop_row_hash(p.drop_seed + static_cast<uint64_t>(bh), i0 + r);
-        named_bar_sync(3 + sg, 128);
-      }
-      const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0);
-      // masked keys: kj >= kv_limit for every query; causal: kj > i0 + c  <=>  c < kj - i0
-      const int c_lo = (kj >= sc.kv_limit) ? kBwdQT : (causal ? kj - i0 : 0);  // first visible query column
-      uint32_t sr[32], dp[32];
-      tmem_ld32_async(tX, sr);
-      tmem_ld32_async(tX + 64, dp);
-      tmem_ld_wait32(sr);
-      tmem_ld_wait32(dp);
-      const uint32_t drow = sDS + sg * Cfg::kDSBytes + r * 128;
-      auto body = [&](auto masked_t) {
-        constexpr bool kMasked = decltype(masked_t)::value;
+    int g0 = 0;
+    for (int n = 0;; ++n) {
+      const int w = take_item(n);
+      if (w < 0) break;
+      const Item it = item(w);
+      const BwdSched& sc = it.sc;
+      const int kj = sc.k0 + r;
+      bool first = true;  // first dS^T store of this warpgroup in this item
+      int g = g0;
+      for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1), ++g) {
+        if ((g & 1) != sg) continue;
+        const int s = g % S;
+        if (p.visited != nullptr && r == 0) {
+          const long long bit = static_cast<long long>(i >> 1) * p.tc + it.j;
+          atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
+        }
+        mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>((g / S) & 1));  // lse2 / D vectors landed
+        mbar_wait(BAR(kBarSFull + sg), static_cast<uint32_t>((g >> 1) & 1));
+        tc_fence_after();
+        if (r == 0 && g == 0) TATN_TRACE_AT(2);
+        if (r == 0 && g == 2) TATN_TRACE_AT(9);
+        const uint64_t* nl2 = reinterpret_cast<const uint64_t*>(vec_gen + s * (Cfg::kVecBytes / 4));  // -lse2 pairs
+        const uint64_t* nD = nl2 + kBwdQT / 2;                                                          // -D pairs
+        const int i0 = i * kBwdQT;
+        if constexpr (DROP) {
+          // the tile's 64 query-row hashes (thread r < 64 computes row i0 + r)
+          named_bar_sync(3 + sg, 128);  // previous tile's hashes fully consumed
+          if (r < kBwdQT) drop_rows[r] = drop_row_hash(p.drop_seed + static_cast<uint64_t>(it.bh), i0 + r);
+          named_bar_sync(3 + sg, 128);
+        }
+        const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0);
+        // masked keys: kj >= kv_limit for every query; causal: kj > i0 + c  <=>  c < kj - i0
+        const int c_lo = (kj >= sc.kv_limit) ? kBwdQT : (causal ? kj - i0 : 0);  // first visible query column
+        uint32_t sr[32], dp[32];
+        tmem_ld32_async(tX, sr);
+        tmem_ld32_async(tX + 64, dp);
+        tmem_ld_wait32(sr);
+        tmem_ld_wait32(dp);
+        const uint32_t drow = sDS + sg * Cfg::kDSBytes + r * 128;
+        auto body = [&](auto masked_t) {
+          constexpr bool kMasked = decltype(masked_t)::value;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          // queries [32*half, 32*half + 32); half 1 is loaded while half 0's results are stored
-          uint32_t pk[16], dk[16];
+          for (int half = 0; half < 2; ++half) {
+            // queries [32*half, 32*half + 32); half 1 is loaded while half 0's results are stored
+            uint32_t pk[16], dk[16];
 #pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2) {
-            const int c4 = half * 32 + 4 * k2;  // four query columns c4 .. c4 + 3
-            const ulonglong2 l4 = *reinterpret_cast<const ulonglong2*>(nl2 + (c4 >> 1));
-            const ulonglong2 d4 = *reinterpret_cast<const ulonglong2*>(nD + (c4 >> 1));
+            for (int k2 = 0; k2 < 8; ++k2) {
+              const int c4 = half * 32 + 4 * k2;  // four query columns c4 .. c4 + 3
+              const ulonglong2 l4 = *reinterpret_cast<const ulonglong2*>(nl2 + (c4 >> 1));
+              const ulonglong2 d4 = *reinterpret_cast<const ulonglong2*>(nD + (c4 >> 1));
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int k = 2 * k2 + e;
-              const int c = c4 + 2 * e;
-              const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sl2x2,
-                                        e ? l4.y : l4.x);
-              float p0, p1;
-              f2_unpack(x, p0, p1);
-              p0 = ex2_approx(p0);
-              p1 = ex2_approx(p1);
-              if constexpr (kMasked) {
-                p0 = (c < c_lo) ? 0.f : p0;
-                p1 = (c + 1 < c_lo) ? 0.f : p1;
-              }
-              const uint64_t nd = e ? d4.y : d4.x;
-              if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
-                float d0, d1;
-                f2_unpack(nd, d0, d1);
-                const float z0 = drop_keep(drop_rows[c], kj, p.drop_thresh) ? p.drop_scale : 0.f;
-                const float z1 = drop_keep(drop_rows[c + 1], kj, p.drop_thresh) ? p.drop_scale : 0.f;
-                dk[k] = pack2<BF16>(p0 * fmaf(__uint_as_float(dp[2 * k]), z0, d0),
-                                    p1 * fmaf(__uint_as_float(dp[2 * k + 1]), z1, d1));
-                pk[k] = pack2<BF16>(p0 * z0, p1 * z1);
-              } else {
-                const uint64_t ds =
-                    f2_mul(f2_pack(p0, p1), f2_add(f2_pack(__uint_as_float(dp[2 * k]), __uint_as_float(dp[2 * k + 1])), nd));
-                float d0, d1;
-                f2_unpack(ds, d0, d1);
-                pk[k] = pack2<BF16>(p0, p1);
-                dk[k] = pack2<BF16>(d0, d1);
+              for (int e = 0; e < 2; ++e) {
+                const int k = 2 * k2 + e;
+                const int c = c4 + 2 * e;
+                const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sl2x2,
+                                          e ? l4.y : l4.x);
+                float p0, p1;
+                f2_unpack(x, p0, p1);
+                p0 = ex2_approx(p0);
+                p1 = ex2_approx(p1);
+                if constexpr (kMasked) {
+                  p0 = (c < c_lo) ? 0.f : p0;
+                  p1 = (c + 1 < c_lo) ? 0.f : p1;
+                }
+                const uint64_t nd = e ? d4.y : d4.x;
+                if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
+                  float d0, d1;
+                  f2_unpack(nd, d0, d1);
+                  const float z0 = drop_keep(drop_rows[c], kj, p.drop_thresh) ? p.drop_scale : 0.f;
+                  const float z1 = drop_keep(drop_rows[c + 1], kj, p.drop_thresh) ? p.drop_scale : 0.f;
+                  dk[k] = pack2<BF16>(p0 * fmaf(__uint_as_float(dp[2 * k]), z0, d0),
+                                      p1 * fmaf(__uint_as_float(dp[2 * k + 1]), z1, d1));
+                  pk[k] = pack2<BF16>(p0 * z0, p1 * z1);
+                } else {
+                  const uint64_t ds = f2_mul(
+                      f2_pack(p0, p1), f2_add(f2_pack(__uint_as_float(dp[2 * k]), __uint_as_float(dp[2 * k + 1])), nd));
+                  float d0, d1;
+                  f2_unpack(ds, d0, d1);
+                  pk[k] = pack2<BF16>(p0, p1);
+                  dk[k] = pack2<BF16>(d0, d1);
+                }
               }
             }
-          }
-          if (half == 0) {
-            tmem_ld32_async(tX + 32, sr);
-            tmem_ld32_async(tX + 96, dp);
-          }
-          tmem_st16(tX + half * 16, pk);       // P^T   -> X cols [0,32)
-          tmem_st16(tX + 64 + half * 16, dk);  // dS^T  -> X cols [64,96)
-          if (half == 0) {
-            // the dQ^T MMA of this warpgroup's previous tile must have released its dS^T buffer
-            mbar_wait(BAR(kBarDSEmpty + sg), dsph ^ 1);
-            dsph ^= 1;
-          }
-          // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
+            if (half == 0) {
+              tmem_ld32_async(tX + 32, sr);
+              tmem_ld32_async(tX + 96, dp);
+            }
+            tmem_st16(tX + half * 16, pk);       // P^T   -> X cols [0,32)
+            tmem_st16(tX + 64 + half * 16, dk);  // dS^T  -> X cols [64,96)
+            if (half == 0) {
+              // the dQ^T MMA of this warpgroup's previous tile must have released its dS^T buffer,
+              // and in a new item the previous item's dK / dV staging must have been stored
+              mbar_wait(BAR(kBarDSEmpty + sg), static_cast<uint32_t>(((g >> 1) & 1) ^ 1));
+              if (first && n > 0) mbar_wait(BAR(kBarStageFree), static_cast<uint32_t>((n - 1) & 1));
+              first = false;
+            }
+            // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const int chunk = half * 4 + cc;
-            st_shared_v4(drow + ((chunk ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+            for (int cc = 0; cc < 4; ++cc) {
+              const int chunk = half * 4 + cc;
+              st_shared_v4(drow + ((chunk ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+            }
+            if (half == 0) {
+              tmem_ld_wait32(sr);
+              tmem_ld_wait32(dp);
+            }
           }
-          if (half == 0) {
-            tmem_ld_wait32(sr);
-            tmem_ld_wait32(dp);
-          }
-        }
-      };
-      if (need_mask) body(std::true_type{});
-      else body(std::false_type{});
-      fence_proxy_async_smem();
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(BAR(kBarPFull + sg));
-      if (r == 0 && idx == 2) TATN_TRACE_AT(10);
+        };
+        if (need_mask) body(std::true_type{});
+        else body(std::false_type{});
+        fence_proxy_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(BAR(kBarPFull + sg));
+        if (r == 0 && g == 2) TATN_TRACE_AT(10);
+      }
+      g0 += it.cnt;
     }
     if (r == 0 && sg == 0) TATN_TRACE_AT(3);
-    // ------------------------------------------------------------ epilogue: warpgroup 0 -> dK, 1 -> dV
-    if (n_iter > 0) {
-      mbar_wait(BAR(kBarFinal), 0);
-      tc_fence_after();
-      if (r == 0 && sg == 0) TATN_TRACE_AT(4);
-    } else {
-      mbar_wait(BAR(kBarKV), 0);  // staging reuses K/V smem
-    }
-    const uint32_t tacc = tmem_base + lane_off + (sg == 0 ? Cfg::kTmemDK : Cfg::kTmemDV);
-    const uint32_t stg = sg == 0 ? sK : sV;
-    const float oscale = sg == 0 ? p.tau : 1.f;  // dK = tau * dS^T Q
-    float* grow_ptr = nullptr;
-    if constexpr (OUT_F32) {
-      grow_ptr = sg == 0 ? p.dk_f32 + static_cast<size_t>(b) * p.k_sb + static_cast<size_t>(h) * p.k_sh +
-                               static_cast<size_t>(kj) * p.k_sn
-                         : p.dv_f32 + static_cast<size_t>(b) * p.v_sb + static_cast<size_t>(h) * p.v_sh +
-                               static_cast<size_t>(kj) * p.v_sn;
-    }
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t v[32];
-      if (n_iter > 0) {
-        tmem_ld32(tacc + c * 32, v);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = 0u;
-      }
-      if constexpr (OUT_F32) {
-        if (kj < p.Nk) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            reinterpret_cast<float4*>(grow_ptr + c * 32)[e] =
-                make_float4(__uint_as_float(v[4 * e]) * oscale, __uint_as_float(v[4 * e + 1]) * oscale,
-                            __uint_as_float(v[4 * e + 2]) * oscale, __uint_as_float(v[4 * e + 3]) * oscale);
-        }
-      } else {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = pack2<BF16>(__uint_as_float(v[2 * e]) * oscale, __uint_as_float(v[2 * e + 1]) * oscale);
-        const int sub = (c * 32) / 64;
-        const int chunk0 = ((c * 32) % 64) / 8;
-        const uint32_t rb = stg + sub * 128 * 128 + r * 128;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          st_shared_v4(rb + (((chunk0 + e) ^ (r & 7)) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
-      }
-    }
-    if constexpr (!OUT_F32) {
-      fence_proxy_async_smem();
-      named_bar_sync(1 + 4 * sg, 128);
-      if (r == 0) {
-        for (int s = 0; s < Cfg::kSubs; ++s) tma_store_4d(sg == 0 ? &tmDK : &tmDV, stg + s * 128 * 128, s * 64, sc.k0, h, b);
-        bulk_commit();
-        bulk_wait_read_all();
-      }
-    }
   } else {
     // ------------------------------------------------------------ dQ warpgroup (warps 8-11)
+    // per Q tile: dQ^T out of TMEM -> fp32 staging -> bulk reduce-add into the workspace;
+    // per item: dK / dV out of TMEM -> 16-bit staging -> TMA store (the softmax warpgroups
+    // meanwhile start the next item)
     const int wq = warp & 3;
-    const int dd = wq * 32 + lane;  // head-dim index == TMEM lane of dQ^T
-    const bool active = dd < D;
+    const int row = wq * 32 + lane;  // TMEM lane: head-dim index of dQ^T, key row of dK / dV
+    const bool active = row < D;
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const float tau = p.tau;
-    uint32_t fph[2] = {0, 0};
-    int idx = 0;
-    for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1)) {
-      const int x = idx & 1;
-      mbar_wait(BAR(kBarDQFull + x), fph[x]);
-      fph[x] ^= 1;
+    const bool leader = warp == 8 && lane == 0;
+    int g = 0;
+    for (int n = 0;; ++n) {
+      const int w = take_item(n);
+      if (w < 0) break;
+      const Item it = item(w);
+      for (int i = it.sc.next(it.sc.i_begin); i < it.sc.i_end; i = it.sc.next(i + 1), ++g) {
+        const int x = g & 1;
+        mbar_wait(BAR(kBarDQFull + x), static_cast<uint32_t>((g >> 1) & 1));
+        tc_fence_after();
+        if (row == 0 && g == 2) TATN_TRACE_AT(12);
+        uint32_t v[64];
+        if (active) {
+          const uint32_t tX = tmem_base + lane_off + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
+          tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        }
+        tc_fence_before();
+        mbar_arrive(BAR(kBarDQEmpty + x));
+        // staging buffer free once the previous bulk reduce has read it
+        if (leader) bulk_wait_read_all();
+        named_bar_sync(2, 128);
+        if (active) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(sDQ + (c * D + row) * 4), "f"(__uint_as_float(v[c]) * tau)
+                         : "memory");
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (leader) {
+          float* dst = p.dq_acc + (static_cast<size_t>(it.bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D;
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                       "r"(sDQ), "r"(Cfg::kDQBytes)
+                       : "memory");
+          bulk_commit();
+          if (g == 2) TATN_TRACE_AT(13);
+        }
+      }
+      // ---------------- item epilogue: dK = tau * acc_K, dV = acc_V
+      mbar_wait(BAR(kBarFinal), static_cast<uint32_t>(n & 1));
       tc_fence_after();
-      if (dd == 0 && idx == 2) TATN_TRACE_AT(12);
-      uint32_t v[64];
-      if (active) {
-        const uint32_t tX = tmem_base + lane_off + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
-        tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-        tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      if (row == 0 && n == 0) TATN_TRACE_AT(4);
+      const int kj = it.sc.k0 + row;
+      if (leader) bulk_wait_read_all();  // the last dQ reduce has read the staging region
+      named_bar_sync(2, 128);
+#pragma unroll 1
+      for (int which = 0; which < 2; ++which) {
+        const uint32_t tacc = tmem_base + lane_off + (which == 0 ? Cfg::kTmemDK : Cfg::kTmemDV);
+        const float oscale = which == 0 ? tau : 1.f;
+        const uint32_t stg = sStage + which * (128 * D * 2);
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t v[32];
+          if (it.cnt > 0) {
+            tmem_ld32(tacc + c * 32, v);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0u;
+          }
+          if constexpr (OUT_F32) {
+            float* gp = which == 0 ? p.dk_f32 + static_cast<size_t>(it.b) * p.k_sb + static_cast<size_t>(it.h) * p.k_sh +
+                                         static_cast<size_t>(kj) * p.k_sn
+                                   : p.dv_f32 + static_cast<size_t>(it.b) * p.v_sb + static_cast<size_t>(it.h) * p.v_sh +
+                                         static_cast<size_t>(kj) * p.v_sn;
+            if (kj < p.Nk) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                reinterpret_cast<float4*>(gp + c * 32)[e] =
+                    make_float4(__uint_as_float(v[4 * e]) * oscale, __uint_as_float(v[4 * e + 1]) * oscale,
+                                __uint_as_float(v[4 * e + 2]) * oscale, __uint_as_float(v[4 * e + 3]) * oscale);
+            }
+          } else {
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              pk[e] = pack2<BF16>(__uint_as_float(v[2 * e]) * oscale, __uint_as_float(v[2 * e + 1]) * oscale);
+            const int sub = (c * 32) / 64;
+            const int chunk0 = ((c * 32) % 64) / 8;
+            const uint32_t rb = stg + sub * 128 * 128 + row * 128;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              st_shared_v4(rb + (((chunk0 + e) ^ (row & 7)) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2],
+                           pk[4 * e + 3]);
+          }
+        }
       }
       tc_fence_before();
-      mbar_arrive(BAR(kBarDQEmpty + x));
-      // staging buffer free once the previous bulk reduce has read it
-      if (warp == 8 && lane == 0) bulk_wait_read_all();
-      named_bar_sync(2, 128);
-      if (active) {
-#pragma unroll
-        for (int c = 0; c < 64; ++c)
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sDQ + (c * D + dd) * 4), "f"(__uint_as_float(v[c]) * tau)
-                       : "memory");
+      mbar_arrive(BAR(kBarAccFree));  // TMEM accumulators may be overwritten by the next item
+      if constexpr (!OUT_F32) {
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (leader) {
+          for (int s = 0; s < Cfg::kSubs; ++s) {
+            tma_store_4d(&tmDK, sStage + s * 128 * 128, s * 64, it.sc.k0, it.h, it.b);
+            tma_store_4d(&tmDV, sStage + 128 * D * 2 + s * 128 * 128, s * 64, it.sc.k0, it.h, it.b);
+          }
+          bulk_commit();
+          bulk_wait_read_all();
+        }
       }
-      fence_proxy_async_smem();
-      named_bar_sync(2, 128);
-      if (warp == 8 && lane == 0) {
-        float* dst = p.dq_acc + (static_cast<size_t>(bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D;
-        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
-                     "r"(sDQ), "r"(Cfg::kDQBytes)
-                     : "memory");
-        bulk_commit();
-        if (idx == 2) TATN_TRACE_AT(13);
-      }
-      ++idx;
+      if (leader) mbar_arrive(BAR(kBarStageFree));
     }
-    if (warp == 8 && lane == 0) bulk_wait_all();
-    if (warp == 8 && lane == 0) TATN_TRACE_AT(8);
+    if (leader) bulk_wait_all();
+    if (leader) TATN_TRACE_AT(8);
   }
 
   tc_fence_before();
@@ -745,6 +835,7 @@ inline void set_dropout(const tatn_attn_desc& d, uint64_t* seed, uint64_t* thres
 }
 cudaEvent_t profile_begin(int which, cudaStream_t s);
 int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm);
+int sm_count();
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows);
 }
@@ -759,12 +850,13 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   float* dq_acc = static_cast<float*>(ws);
   float* lse2 = dq_acc + rows * D;
   float* delta = lse2 + rows;
+  int* item_counter = reinterpret_cast<int*>(delta + rows);
   {
     const long long threads = static_cast<long long>(rows) * (D / 8);
     const int blocks = static_cast<int>((threads + 255) / 256);
     tatn_dev::tatn_bwd_pre<D, BF16, OUT_F32><<<blocks, 256, 0, stream>>>(
         o, static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
-        d.H, d.Nq, Nq_pad, lse2, delta, dq_acc);
+        d.H, d.Nq, Nq_pad, lse2, delta, dq_acc, item_counter);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -793,6 +885,8 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.delta = delta;
   p.dq_acc = dq_acc;
   p.n_ktiles = p.tc;
+  p.n_items = d.B * d.H * p.n_ktiles;
+  p.item_counter = item_counter;
   p.group = tatn_host::schedule_group(d.B * d.H, p.n_ktiles, static_cast<double>(d.Nq) * D * 8.0, 1);
   p.dk_f32 = OUT_F32 ? static_cast<float*>(dk) : nullptr;
   p.dv_f32 = OUT_F32 ? static_cast<float*>(dv) : nullptr;
@@ -810,7 +904,10 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(static_cast<unsigned>(d.B * d.H * p.n_ktiles));
+  // dense: persistent, one CTA per SM looping over items; block-sparse: one CTA per item
+  // (the grid column is read once into a shared-memory bitmask)
+  const int n_sm = tatn_host::sm_count();
+  dim3 grid(static_cast<unsigned>(d.block_grid != nullptr ? p.n_items : std::min(p.n_items, n_sm)));
   cudaEvent_t prof_stop = tatn_host::profile_begin(1, stream);
   kern<<<grid, tatn_dev::kBwdThreads, Cfg::kSmemBytes, stream>>>(mq, mk, mv, mdo, mdk, mdv, p, lse2, Nq_pad);
   if (prof_stop) cudaEventRecord(prof_stop, stream);

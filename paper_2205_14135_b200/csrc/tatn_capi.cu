@@ -167,6 +167,16 @@ int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int 
   g = std::min(g, std::max(1, l2_cap));
   return std::max(1, std::min(g, heads));
 }
+int sm_count() {
+  static int n = 0;  // benign race: idempotent
+  if (n == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      n = v;
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows) {
   return make_map_4d(map, tma_dtype(dtype), 2, base, d, n, H, B, str, box_rows);
@@ -301,9 +311,10 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
 
 size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc) {
   if (validate(desc) != TATN_OK) return 0;
-  // dQ accumulator [B,H,Nq_pad,d] fp32 + lse2 [B,H,Nq_pad] + D [B,H,Nq_pad], Nq_pad = roundup(Nq, 128)
+  // dQ accumulator [B,H,Nq_pad,d] fp32 + lse2 [B,H,Nq_pad] + D [B,H,Nq_pad], Nq_pad = roundup(Nq, 128),
+  // + the persistent backward's item counter
   const size_t rows = static_cast<size_t>(desc->B) * desc->H * ((desc->Nq + 127) / 128 * 128);
-  return rows * desc->d * sizeof(float) + 2 * rows * sizeof(float);
+  return rows * desc->d * sizeof(float) + 2 * rows * sizeof(float) + 16;  // + K3 item counter
 }
 
 int tatn_bwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, const void* o, const void* dO,

@@ -40,6 +40,8 @@ struct BwdParams {
   float* delta;      // [B, H, Nq] workspace: D_i = rowsum(dO_i * O_i)
   float* dq_acc;     // [B, H, Nq, d] fp32 workspace
   int n_ktiles;      // ceil(Nk / 128)
+  int n_items;       // B * H * n_ktiles work items (one 128-key tile of one head each)
+  int* item_counter; // persistent schedule: next unclaimed item (zeroed by K2 every launch)
   int group;         // heads per scheduling group (CTA order, see tatn_bwd_kernel)
   uint64_t drop_seed;   // dropout (see FwdParams)
   uint64_t drop_thresh;

@@ -112,5 +112,5 @@ def test_workspace_formula():
     lib = _lib.load()
     d = good_desc()
     rows = 2 * 3 * 384  # Nq padded to a multiple of 128
-    assert lib.tatn_bwd_workspace_bytes(ctypes.byref(d)) == rows * 64 * 4 + 2 * rows * 4
+    assert lib.tatn_bwd_workspace_bytes(ctypes.byref(d)) == rows * 64 * 4 + 2 * rows * 4 + 16
     assert lib.tatn_bwd_workspace_bytes(ctypes.byref(good_desc(B=0))) == 0
