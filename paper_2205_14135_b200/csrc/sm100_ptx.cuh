@@ -431,5 +431,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                      \
   } while (0)
 #endif
+// per-event SM clock trace of CTA 0 (debug builds only): slot `ev` of Q tile g
+#ifdef TATN_TRACE
+// TATN_EV_INIT caches the trace pointer in a register (a global load per event would
+// perturb the timeline it measures)
+#define TATN_EV_INIT() unsigned long long* const tatn_ev_buf = (blockIdx.x == 0) ? g_tatn_trace : nullptr
+#define TATN_EV(g, ev)                                                                                   \
+  do {                                                                                                   \
+    if (tatn_ev_buf && (g) < 1024)                                                                       \
+      tatn_ev_buf[200000ull * 16 + static_cast<unsigned long long>(g) * 8 + (ev)] = clock64();           \
+  } while (0)
+#else
+#define TATN_EV_INIT() \
+  do {                 \
+  } while (0)
+#define TATN_EV(g, ev) \
+  do {                 \
+  } while (0)
+#endif
 
 }  // namespace tatn_dev

@@ -36,6 +36,10 @@
 #include "sm100_ptx.cuh"
 #include "tatn_params.h"
 
+#ifndef TATN_DQ_RED
+#define TATN_DQ_RED 1  // dQ partials: red.global.add from registers (1) or smem staging + bulk reduce (0)
+#endif
+
 namespace tatn_dev {
 
 constexpr int kBwdThreads = 448;
@@ -75,6 +79,13 @@ struct BwdCfg {
   // front (S^T into X_x) need not wait for the dQ warpgroup to drain dQ^T out of X_x.
   static constexpr bool kSepDQ = (D == 64);
   static constexpr uint32_t kTmemDQ = 384;  // [384 + 64x, 448 + 64x) when kSepDQ
+  // dQ partials by red.global.add from registers (d = 64: frees the shared-memory port of
+  // the staging write + bulk-reduce read); d = 128 keeps smem staging + one bulk reduce,
+  // which measured faster there (r01 sweep)
+  static constexpr bool kDQRed = TATN_DQ_RED && D == 64;
+  // d = 64: dQ^T by an M = 64 MMA. Its rows live in TMEM lanes 0-15 of each 32-lane
+  // quadrant (row = 16 * quadrant + lane).
+  static constexpr bool kDQ64 = D == 64;
 };
 
 struct BwdSched {
@@ -303,6 +314,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int lane = static_cast<int>(lane_id());
   uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
   if (threadIdx.x == 0) TATN_TRACE_AT(0);
+  TATN_EV_INIT();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
@@ -430,7 +442,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     constexpr uint32_t ab = BF16 ? 1u : 0u;
     constexpr uint32_t idesc_s = make_idesc_f16(ab, 128, kBwdQT, 0, 0);   // S^T, dP^T
     constexpr uint32_t idesc_acc = make_idesc_f16(ab, 128, D, 0, 1);      // dV, dK (B MN-major)
-    constexpr uint32_t idesc_dq = make_idesc_f16(ab, 128, kBwdQT, 1, 1);  // dQ^T (A, B MN-major)
+    // dQ^T (A, B MN-major): M = d; at d = 64 an M = 64 MMA (half the A bytes of M = 128)
+    constexpr uint32_t idesc_dq = make_idesc_f16(ab, Cfg::kDQ64 ? 64 : 128, kBwdQT, 1, 1);
     // base descriptors; per-MMA operands add (byte offset >> 4) to the start-address field
     const uint64_t dKV0 = make_sdesc_sw128(sKV, 16, 1024);               // K / V as K-major A
     const uint64_t dQk0 = make_sdesc_sw128(sQ, 16, 1024);                // Q as K-major B
@@ -463,8 +476,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t offa = voff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
             const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+#ifdef TATN_EXP_TS_FRONT  // timing experiment only: A operand from (garbage) TMEM
+            mma_ts(tmem_base + Cfg::kTmemX + x * 128 + 64, tmem_base + Cfg::kTmemDQ + kk * 8,
+                   dDOk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
+            (void)offa;
+#else
             mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, dKV0 + (offa >> 4),
                    dDOk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
+#endif
           }
         }
         __syncwarp();
@@ -477,12 +496,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t offa = koff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
             const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+#ifdef TATN_EXP_TS_FRONT
+            mma_ts(tmem_base + Cfg::kTmemX + x * 128, tmem_base + Cfg::kTmemDQ + 32 + kk * 8,
+                   dQk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
+            (void)offa;
+#else
             mma_ss(tmem_base + Cfg::kTmemX + x * 128, dKV0 + (offa >> 4), dQk0 + ((s * Cfg::kQTile + offb) >> 4),
                    idesc_s, kk > 0 ? 1u : 0u);
+#endif
           }
           mma_commit(BAR(kBarSFull + x));
         }
         __syncwarp();
+        if (lane == 0) TATN_EV(g, 3);
       };
       auto wait_dq_drained = [&](int g) {  // dQ^T of Q tile g read out of its TMEM buffer
         mbar_wait(BAR(kBarDQEmpty + (g & 1)), static_cast<uint32_t>((g >> 1) & 1));
@@ -500,6 +526,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int s = g % S;
         mbar_wait(BAR(kBarPFull + x), static_cast<uint32_t>((g >> 1) & 1));
         tc_fence_after();
+        if (lane == 0) TATN_EV(g, 2);
         if (i == 0 && n > 0) {
           mbar_wait(BAR(kBarAccFree), static_cast<uint32_t>((n - 1) & 1));  // previous dK / dV drained
           tc_fence_after();
@@ -532,6 +559,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mma_commit(BAR(kBarDSEmpty + x));
           }
           __syncwarp();
+          if (lane == 0) TATN_EV(g, 4);
         };
         if constexpr (Cfg::kSepDQ) {
           // X_x is free once dV/dK have read P^T / dS^T (in-order pipe): start the next front
@@ -585,8 +613,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
         }
         mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>((g / S) & 1));  // lse2 / D vectors landed
+        if (r == 0) TATN_EV(g, 7);
         mbar_wait(BAR(kBarSFull + sg), static_cast<uint32_t>((g >> 1) & 1));
         tc_fence_after();
+        if (r == 0) TATN_EV(g, 0);
         if (r == 0 && g == 0) TATN_TRACE_AT(2);
         if (r == 0 && g == 2) TATN_TRACE_AT(9);
         const uint64_t* nl2 = reinterpret_cast<const uint64_t*>(vec_gen + s * (Cfg::kVecBytes / 4));  // -lse2 pairs
@@ -682,6 +712,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(BAR(kBarPFull + sg));
+        if (r == 0) TATN_EV(g, 1);
         if (r == 0 && g == 2) TATN_TRACE_AT(10);
       }
       g0 += it.cnt;
@@ -693,8 +724,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // per item: dK / dV out of TMEM -> 16-bit staging -> TMA store (the softmax warpgroups
     // meanwhile start the next item)
     const int wq = warp & 3;
-    const int row = wq * 32 + lane;  // TMEM lane: head-dim index of dQ^T, key row of dK / dV
-    const bool active = row < D;
+    const int row = wq * 32 + lane;  // TMEM lane: key row of dK / dV
+    // head-dim index of dQ^T held by this thread's TMEM lane
+    const int dd = Cfg::kDQ64 ? wq * 16 + lane : row;
+    const bool active = Cfg::kDQ64 ? lane < 16 : row < D;
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const float tau = p.tau;
     const bool leader = warp == 8 && lane == 0;
@@ -707,9 +740,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int x = g & 1;
         mbar_wait(BAR(kBarDQFull + x), static_cast<uint32_t>((g >> 1) & 1));
         tc_fence_after();
+        if (row == 0) TATN_EV(g, 5);
         if (row == 0 && g == 2) TATN_TRACE_AT(12);
         uint32_t v[64];
-        if (active) {
+        if (Cfg::kDQ64 || active) {  // warp-uniform: tcgen05.ld is .sync.aligned
           const uint32_t tX = tmem_base + lane_off + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
           tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
           tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
@@ -717,12 +751,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         mbar_arrive(BAR(kBarDQEmpty + x));
         // staging buffer free once the previous bulk reduce has read it
+#ifdef TATN_EXP_NO_DQ
+        if (true) continue;  // timing experiment only: skip the dQ staging and reduction
+#endif
+        if constexpr (Cfg::kDQRed) {
+        // fire-and-forget fp32 reductions straight from registers into the L2-resident
+        // accumulator: lanes hold consecutive head-dim columns, so each instruction is one
+        // coalesced 64-byte reduction, and no shared-memory bandwidth is spent on dQ
+        if (active) {
+          float* dst = p.dq_acc + (static_cast<size_t>(it.bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D + dd;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) atomicAdd(dst + c * D, __uint_as_float(v[c]) * tau);
+        }
+        continue;
+        }
         if (leader) bulk_wait_read_all();
         named_bar_sync(2, 128);
         if (active) {
 #pragma unroll
           for (int c = 0; c < 64; ++c)
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(sDQ + (c * D + row) * 4), "f"(__uint_as_float(v[c]) * tau)
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(sDQ + (c * D + dd) * 4), "f"(__uint_as_float(v[c]) * tau)
                          : "memory");
         }
         fence_proxy_async_smem();
@@ -733,6 +781,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        "r"(sDQ), "r"(Cfg::kDQBytes)
                        : "memory");
           bulk_commit();
+          TATN_EV(g, 6);
           if (g == 2) TATN_TRACE_AT(13);
         }
       }
