@@ -36,6 +36,9 @@
 #include "sm100_ptx.cuh"
 #include "tatn_params.h"
 
+#ifndef TATN_BWD_SPLIT
+#define TATN_BWD_SPLIT 0  // softmax warpgroups split each Q tile's columns (1) or alternate tiles (0)
+#endif
 #ifndef TATN_DQ_RED
 #define TATN_DQ_RED 1  // dQ partials: red.global.add from registers (1) or smem staging + bulk reduce (0)
 #endif
@@ -86,6 +89,7 @@ struct BwdCfg {
   // d = 64: dQ^T by an M = 64 MMA. Its rows live in TMEM lanes 0-15 of each 32-lane
   // quadrant (row = 16 * quadrant + lane).
   static constexpr bool kDQ64 = D == 64;
+  static constexpr bool kSplit = TATN_BWD_SPLIT != 0;
 };
 
 struct BwdSched {
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
     for (int x = 0; x < 2; ++x) {
-      mbar_init(BAR(kBarPFull + x), 128);
+      mbar_init(BAR(kBarPFull + x), Cfg::kSplit ? 256 : 128);
       mbar_init(BAR(kBarDQEmpty + x), 128);
     }
     mbar_init(BAR(kBarAccFree), 128);
@@ -588,13 +592,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax warpgroups
-    const int sg = warp >> 2;               // warpgroup = X buffer = parity of its Q tiles
+    // kSplit: both warpgroups work on every Q tile, warpgroup sg on query columns
+    // [32 sg, 32 sg + 32) (halves the per-tile latency of the softmax step); otherwise
+    // warpgroup sg takes the Q tiles of parity sg (ping-pong over the two X buffers).
+    constexpr bool kSplit = Cfg::kSplit;
+    const int sg = warp >> 2;
     const int r = (warp & 3) * 32 + lane;   // key row within tile == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const float sl2 = p.scale_log2;
     const uint64_t sl2x2 = f2_pack(sl2, sl2);
     const bool causal = p.mask_kind == kMaskCausal;
-    const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + sg * 128;
     uint64_t* drop_rows = reinterpret_cast<uint64_t*>(smem_gen + Cfg::kOffDrop + sg * 512);
     int g0 = 0;
     for (int n = 0;; ++n) {
@@ -606,15 +613,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       bool first = true;  // first dS^T store of this warpgroup in this item
       int g = g0;
       for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1), ++g) {
-        if ((g & 1) != sg) continue;
+        if (!kSplit && (g & 1) != sg) continue;
         const int s = g % S;
+        const int x = g & 1;  // X buffer (== sg without kSplit)
+        const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + x * 128;
         if (p.visited != nullptr && r == 0) {
           const long long bit = static_cast<long long>(i >> 1) * p.tc + it.j;
           atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
         }
         mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>((g / S) & 1));  // lse2 / D vectors landed
         if (r == 0) TATN_EV(g, 7);
-        mbar_wait(BAR(kBarSFull + sg), static_cast<uint32_t>((g >> 1) & 1));
+        mbar_wait(BAR(kBarSFull + x), static_cast<uint32_t>((g >> 1) & 1));
         tc_fence_after();
         if (r == 0) TATN_EV(g, 0);
         if (r == 0 && g == 0) TATN_TRACE_AT(2);
@@ -631,16 +640,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0);
         // masked keys: kj >= kv_limit for every query; causal: kj > i0 + c  <=>  c < kj - i0
         const int c_lo = (kj >= sc.kv_limit) ? kBwdQT : (causal ? kj - i0 : 0);  // first visible query column
+        constexpr int kH0 = 0, kH1 = kSplit ? 1 : 2;  // halves (32 query columns) per warpgroup
+        const int hbase = kSplit ? sg : 0;
         uint32_t sr[32], dp[32];
-        tmem_ld32_async(tX, sr);
-        tmem_ld32_async(tX + 64, dp);
+        tmem_ld32_async(tX + 32 * hbase, sr);
+        tmem_ld32_async(tX + 64 + 32 * hbase, dp);
         tmem_ld_wait32(sr);
         tmem_ld_wait32(dp);
-        const uint32_t drow = sDS + sg * Cfg::kDSBytes + r * 128;
+        const uint32_t drow = sDS + x * Cfg::kDSBytes + r * 128;
         auto body = [&](auto masked_t) {
           constexpr bool kMasked = decltype(masked_t)::value;
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
+          for (int hh = kH0; hh < kH1; ++hh) {
+            const int half = hbase + hh;
             // queries [32*half, 32*half + 32); half 1 is loaded while half 0's results are stored
             uint32_t pk[16], dk[16];
 #pragma unroll
@@ -652,10 +664,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               for (int e = 0; e < 2; ++e) {
                 const int k = 2 * k2 + e;
                 const int c = c4 + 2 * e;
-                const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sl2x2,
-                                          e ? l4.y : l4.x);
+                const uint64_t xv = f2_fma(f2_pack(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sl2x2,
+                                           e ? l4.y : l4.x);
                 float p0, p1;
-                f2_unpack(x, p0, p1);
+                f2_unpack(xv, p0, p1);
                 p0 = ex2_approx(p0);
                 p1 = ex2_approx(p1);
                 if constexpr (kMasked) {
@@ -681,16 +693,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
               }
             }
-            if (half == 0) {
+            if (!kSplit && hh == 0) {
               tmem_ld32_async(tX + 32, sr);
               tmem_ld32_async(tX + 96, dp);
             }
             tmem_st16(tX + half * 16, pk);       // P^T   -> X cols [0,32)
             tmem_st16(tX + 64 + half * 16, dk);  // dS^T  -> X cols [64,96)
-            if (half == 0) {
-              // the dQ^T MMA of this warpgroup's previous tile must have released its dS^T buffer,
-              // and in a new item the previous item's dK / dV staging must have been stored
-              mbar_wait(BAR(kBarDSEmpty + sg), static_cast<uint32_t>(((g >> 1) & 1) ^ 1));
+            if (hh == 0) {
+              // the dQ^T MMA of tile g - 2 must have released the dS^T buffer, and in a new
+              // item the previous item's dK / dV staging must have been stored
+              mbar_wait(BAR(kBarDSEmpty + x), static_cast<uint32_t>(((g >> 1) & 1) ^ 1));
               if (first && n > 0) mbar_wait(BAR(kBarStageFree), static_cast<uint32_t>((n - 1) & 1));
               first = false;
             }
@@ -700,7 +712,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               const int chunk = half * 4 + cc;
               st_shared_v4(drow + ((chunk ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
             }
-            if (half == 0) {
+            if (!kSplit && hh == 0) {
               tmem_ld_wait32(sr);
               tmem_ld_wait32(dp);
             }
@@ -711,7 +723,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(BAR(kBarPFull + sg));
+        mbar_arrive(BAR(kBarPFull + x));
         if (r == 0) TATN_EV(g, 1);
         if (r == 0 && g == 2) TATN_TRACE_AT(10);
       }
