@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TATN_B200_ABI_VERSION 2
+#define TATN_B200_ABI_VERSION 3
 
 typedef enum {
   TATN_OK = 0,
@@ -52,9 +52,14 @@ typedef enum { TATN_DTYPE_BF16 = 0, TATN_DTYPE_FP16 = 1 } tatn_dtype;
 typedef enum { TATN_OUT_INPUT_DTYPE = 0, TATN_OUT_FP32 = 1 } tatn_out_dtype;
 
 /* tatn::MaskKind (attn_config.hpp:12). Causal masks key j > query i;
- * KeyPadding masks key j >= valid_len[b] (attn_config.cpp:20-32). Custom n x n
- * masks are not on the device path (TATN_E_UNSUPPORTED). */
-typedef enum { TATN_MASK_NONE = 0, TATN_MASK_CAUSAL = 1, TATN_MASK_KEY_PADDING = 2 } tatn_mask_kind;
+ * KeyPadding masks key j >= valid_len[b]; Custom masks (i, j) where the additive
+ * pattern is -inf (attn_config.cpp:20-32), given as the bit-packed custom_mask below. */
+typedef enum {
+  TATN_MASK_NONE = 0,
+  TATN_MASK_CAUSAL = 1,
+  TATN_MASK_KEY_PADDING = 2,
+  TATN_MASK_CUSTOM = 3
+} tatn_mask_kind;
 
 typedef struct {
   int32_t B, H;      /* independent (batch, head) slices                          */
@@ -82,6 +87,14 @@ typedef struct {
    * so a one-head call reproduces the reference's mask bit for bit. p_drop in [0, 1). */
   double p_drop;
   uint64_t seed;
+  /* Custom mask (MaskSpec::custom_additive, attn_config.hpp:27; ABI v3): bit-packed keep
+   * matrix in DEVICE memory, row-major [Nq][custom_words] uint32 per batch element: bit
+   * (j & 31) of word (j >> 5) of row i is 1 iff custom(i, j) == 0 (keep), 0 iff -inf.
+   * custom_words >= ceil(Nk/32) and a multiple of 4; custom_bstride = words between batch
+   * elements (0: one mask shared by every slice). NULL unless mask_kind == CUSTOM. */
+  const uint32_t* custom_mask;
+  int32_t custom_words;
+  int64_t custom_bstride;
 } tatn_attn_desc;
 
 /* Host-only descriptor check (no device access); same codes as the compute calls. */
@@ -93,7 +106,8 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
              float* lse, void* stream);
 
 /* Workspace for tatn_bwd: fp32 dQ accumulator [B,H,Nq_pad,d] + lse2 and D vectors
- * [B,H,Nq_pad], Nq_pad = Nq rounded up to 128, + 16 bytes (persistent scheduler counter). */
+ * [B,H,Nq_pad], Nq_pad = Nq rounded up to 128, + 16 bytes (persistent scheduler counter)
+ * + for CUSTOM masks the transposed bit mask [B or 1][Nk][Nq_pad/32] uint32. */
 size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc);
 
 /* Backward with recomputation from lse (Algorithm 4).

@@ -28,7 +28,8 @@ LIB = HERE / "liboracle.so"
 REF_LIB = HERE / "_ref" / "libtatn_ref.so"
 
 MASK_NONE, MASK_CAUSAL, MASK_KEY_PADDING = 0, 1, 2
-MASK_CODES = {"none": MASK_NONE, "causal": MASK_CAUSAL, "key_padding": MASK_KEY_PADDING}
+MASK_CUSTOM = 3
+MASK_CODES = {"none": MASK_NONE, "causal": MASK_CAUSAL, "key_padding": MASK_KEY_PADDING, "custom": MASK_CUSTOM}
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -51,6 +52,8 @@ class OrcCfg(ctypes.Structure):
         ("tc", ctypes.c_int),
         ("p_drop", ctypes.c_double),
         ("seed", ctypes.c_uint64),
+        ("custom", ctypes.c_void_p),
+        ("custom_stride", ctypes.c_longlong),
     ]
 
 
@@ -134,6 +137,10 @@ def ref() -> ctypes.CDLL:
         R.ref_memeff_backward.restype = i
         R.ref_time_fwd_bwd.argtypes = [i, i, i, i, i, i]
         R.ref_time_fwd_bwd.restype = ctypes.c_double
+        R.ref_write_matrix.argtypes = [ctypes.c_char_p, i, i, i, _dp]
+        R.ref_write_matrix.restype = i
+        R.ref_read_matrix.argtypes = [ctypes.c_char_p, i, ctypes.POINTER(i), ctypes.POINTER(i), _dp, ctypes.c_longlong]
+        R.ref_read_matrix.restype = i
         _ref = R
     return _ref
 
@@ -181,8 +188,17 @@ def round_to(x: np.ndarray, dtype: str) -> np.ndarray:
 
 
 # ----------------------------------------------------------------------------- attention
-def _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc, p_drop=0.0, seed=0):
+def _custom_u8(custom, shape):
+    """Custom keep-mask (True/1 = keep) broadcast to `shape` as contiguous uint8 (kept alive by the caller)."""
+    if custom is None:
+        return None
+    return np.ascontiguousarray(np.broadcast_to(np.asarray(custom).astype(np.uint8), shape))
+
+
+def _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc, p_drop=0.0, seed=0, custom=None, custom_stride=0):
     c = OrcCfg()
+    if custom is not None:
+        c.custom, c.custom_stride = custom.ctypes.data, int(custom_stride)
     c.p_drop, c.seed = float(p_drop), int(seed)
     c.n, c.nk, c.d = Nq, Nk, d
     c.tau = tau if tau is not None else 1.0 / math.sqrt(d)
@@ -199,15 +215,18 @@ def _contig(*arrs):
     return [np.ascontiguousarray(a, dtype=np.float64) for a in arrs]
 
 
-def forward(q, k, v, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None, p_drop=0.0, seed=0):
+def forward(q, k, v, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None, p_drop=0.0, seed=0,
+            custom=None):
     """O, LSE for q [B,H,Nq,d], k/v [B,H,Nk,d]. valid_len: per-batch array or scalar.
-    Dropout: slice (b, h) uses seed + b*H + h, the C ABI's batched convention."""
+    Dropout: slice (b, h) uses seed + b*H + h, the C ABI's batched convention.
+    custom (mask="custom"): keep-mask broadcastable to [B, H, Nq, Nk] (True = keep)."""
     q, k, v = _contig(q, k, v)
     B, H, Nq, d = q.shape
     Nk = k.shape[2]
     if grid is not None:
         grid = np.ascontiguousarray(grid, dtype=np.uint8)
-    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc, p_drop, seed)
+    cu = _custom_u8(custom, (B, H, Nq, Nk))
+    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc, p_drop, seed, cu, Nq * Nk)
     vl = None
     if valid_len is not None:
         vl = np.ascontiguousarray(np.broadcast_to(np.asarray(valid_len, dtype=np.int32).reshape(-1, 1), (B, H)).reshape(-1))
@@ -220,14 +239,15 @@ def forward(q, k, v, tau=None, mask="none", valid_len=None, grid=None, br=128, b
     return o, lse
 
 
-def forward_rows(q, k, v, rows, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128):
+def forward_rows(q, k, v, rows, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, custom=None):
     """Forward on one slice (q [Nq,d]) restricted to the given query rows."""
     q, k, v = _contig(q, k, v)
     Nq, d = q.shape
     Nk = k.shape[0]
     if grid is not None:
         grid = np.ascontiguousarray(grid, dtype=np.uint8)
-    c = _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc)
+    cu = _custom_u8(custom, (Nq, Nk))
+    c = _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc, custom=cu)
     rows = np.ascontiguousarray(rows, dtype=np.int32)
     o = np.zeros_like(q)
     lse = np.zeros(Nq)
@@ -239,14 +259,15 @@ def forward_rows(q, k, v, rows, tau=None, mask="none", valid_len=None, grid=None
 
 
 def backward_dq_rows(q, k, v, o_rows, do, lse_rows, rows, tau=None, mask="none", valid_len=None, grid=None, br=128,
-                     bc=128):
+                     bc=128, custom=None):
     """dQ for the given query rows of one slice; o_rows / lse_rows are those rows' forward outputs."""
     q, k, v, o_rows, do, lse_rows = _contig(q, k, v, o_rows, do, lse_rows)
     Nq, d = q.shape
     Nk = k.shape[0]
     if grid is not None:
         grid = np.ascontiguousarray(grid, dtype=np.uint8)
-    c = _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc)
+    cu = _custom_u8(custom, (Nq, Nk))
+    c = _cfg(Nq, Nk, d, tau, mask, valid_len, grid, br, bc, custom=cu)
     rows = np.ascontiguousarray(rows, dtype=np.int32)
     out = np.empty((len(rows), d))
     lib().orc_backward_dq_rows(ctypes.byref(c), _ptr(q), _ptr(k), _ptr(v), _ptr(o_rows), _ptr(do), _ptr(lse_rows),
@@ -254,14 +275,16 @@ def backward_dq_rows(q, k, v, o_rows, do, lse_rows, rows, tau=None, mask="none",
     return out
 
 
-def backward(q, k, v, o, do, lse, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None, p_drop=0.0, seed=0):
+def backward(q, k, v, o, do, lse, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, threads=None, p_drop=0.0, seed=0,
+             custom=None):
     """dQ, dK, dV from the saved (o, lse) — Algorithm 4 semantics in fp64."""
     q, k, v, o, do, lse = _contig(q, k, v, o, do, lse)
     B, H, Nq, d = q.shape
     Nk = k.shape[2]
     if grid is not None:
         grid = np.ascontiguousarray(grid, dtype=np.uint8)
-    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc, p_drop, seed)
+    cu = _custom_u8(custom, (B, H, Nq, Nk))
+    c = _cfg(Nq, Nk, d, tau, mask, None, grid, br, bc, p_drop, seed, cu, Nq * Nk)
     vl = None
     if valid_len is not None:
         vl = np.ascontiguousarray(np.broadcast_to(np.asarray(valid_len, dtype=np.int32).reshape(-1, 1), (B, H)).reshape(-1))
@@ -341,22 +364,43 @@ def ref_gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
     return out
 
 
+def ref_write_matrix(path, m: np.ndarray, binary: bool) -> None:
+    """The reference's write_matrix_binary / write_matrix_csv (matrix_io.cpp:116-172)."""
+    a = np.ascontiguousarray(m, dtype=np.float64)
+    if ref().ref_write_matrix(os.fspath(path).encode(), int(binary), a.shape[0], a.shape[1], _ptr(a)) != 0:
+        raise RuntimeError(f"reference matrix write failed: {path}")
+
+
+def ref_read_matrix(path, binary: bool, capacity: int = 1 << 22) -> np.ndarray:
+    """The reference's read_matrix_binary / read_matrix_csv; raises on the reference's errors."""
+    out = np.empty(capacity, dtype=np.float64)
+    r, c = ctypes.c_int(0), ctypes.c_int(0)
+    st = ref().ref_read_matrix(os.fspath(path).encode(), int(binary), ctypes.byref(r), ctypes.byref(c), _ptr(out),
+                               capacity)
+    if st != 0:
+        raise RuntimeError(f"reference matrix read failed ({st}): {path}")
+    return out[: r.value * c.value].reshape(r.value, c.value).copy()
+
+
 def ref_dropout_scale(seed: int, i: int, j: int, p: float) -> float:
     return float(ref().ref_dropout_scale(seed, i, j, p))
 
 
 def ref_standard(q, k, v, do=None, tau=None, mask="none", valid_len=None, grid=None, br=128, bc=128, p_drop=0.0,
-                 seed=0):
+                 seed=0, custom=None):
     """The reference's standard_forward (+ standard_backward) on one slice.
-    Returns dict with o, lse, m, l, fwd_counters (+ dq, dk, dv, bwd_counters)."""
+    Returns dict with o, lse, m, l, fwd_counters (+ dq, dk, dv, bwd_counters).
+    mask="custom": `custom` is the [n, nk] keep matrix (MaskSpec::custom_additive)."""
     q, k, v = _contig(q, k, v)
     n, d = q.shape
     nk = k.shape[0]
     tau = tau if tau is not None else 1.0 / math.sqrt(d)
     mk = MASK_CODES[mask] if isinstance(mask, str) else int(mask)
     vl = int(valid_len) if valid_len is not None else nk
+    if mk == MASK_CUSTOM:
+        grid = np.ascontiguousarray(np.broadcast_to(np.asarray(custom).astype(np.uint8), (n, nk)))
     g = np.ascontiguousarray(grid, dtype=np.uint8) if grid is not None else None
-    tc = g.shape[1] if g is not None else 0
+    tc = nk if mk == MASK_CUSTOM else (g.shape[1] if g is not None else 0)
     gp = _ptr(g, _u8p) if g is not None else None
     o = np.empty_like(q)
     lse = np.empty(n); m = np.empty(n); l = np.empty(n)

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <exception>
 #include <limits>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -19,6 +20,7 @@
 #include "tatn/dropout.hpp"
 #include "tatn/counters.hpp"
 #include "tatn/matrix.hpp"
+#include "tatn/matrix_io.hpp"
 #include "tatn/random.hpp"
 #include "tatn/reference.hpp"
 #include "tatn/softmax.hpp"
@@ -45,6 +47,17 @@ tatn::AttnConfig make_cfg(int n, int d, double tau, int mask_kind, int valid_len
   cfg.seed = seed;
   if (mask_kind == 1) cfg.mask = tatn::MaskSpec::causal();
   if (mask_kind == 2) cfg.mask = tatn::MaskSpec::key_padding(valid_len);
+  if (mask_kind == 3) {
+    // Custom: `grid` carries an n x nk keep matrix (1 = 0.0, 0 = -inf); the reference wants
+    // an n x n additive pattern (attn_config.cpp:50-52), keys >= nk are never read
+    const double ninf = -std::numeric_limits<double>::infinity();
+    tatn::Matrix pat(n, n);
+    const int nk = tc;  // mask_kind 3 passes nk in tc
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) pat(i, j) = (j < nk && grid[static_cast<size_t>(i) * nk + j]) ? 0.0 : ninf;
+    cfg.mask = tatn::MaskSpec::custom_additive(std::move(pat));
+    return cfg;
+  }
   if (grid != nullptr) {
     const double ninf = -std::numeric_limits<double>::infinity();
     tatn::Matrix pat(n, n);
@@ -203,4 +216,29 @@ double ref_time_fwd_bwd(int nslices, int n, int d, int mask_kind, int memeff, in
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+
+// The reference's matrix_io (matrix_io.cpp): write rows x cols binary64 values as TATN binary
+// (binary != 0) or 17-digit CSV to `path`; read one back into `out` (capacity rows*cols).
+int ref_write_matrix(const char* path, int binary, int rows, int cols, const double* data) {
+  try {
+    const auto m = to_matrix(data, rows, cols);
+    if (binary) tatn::write_matrix_binary(m, std::string(path));
+    else tatn::write_matrix_csv(m, std::string(path));
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+int ref_read_matrix(const char* path, int binary, int* rows, int* cols, double* out, long long capacity) {
+  try {
+    const auto m = binary ? tatn::read_matrix_binary(std::string(path)) : tatn::read_matrix_csv(std::string(path));
+    *rows = static_cast<int>(m.rows());
+    *cols = static_cast<int>(m.cols());
+    if (static_cast<long long>(m.rows() * m.cols()) > capacity) return -2;
+    from_matrix(m, out);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
 }  // extern "C"

@@ -15,6 +15,8 @@ _PKG = Path(__file__).resolve().parent
 # TATN_B200_LIB may point at an alternative in-tree build (tuning experiments); default is the product library
 LIB_PATH = Path(os.environ.get("TATN_B200_LIB", _PKG / "lib" / "libtatn_b200.so"))
 
+ABI_VERSION = 3  # TATN_B200_ABI_VERSION (include/tatn_b200.h)
+
 TATN_OK = 0
 TATN_E_ARG = 1
 TATN_E_SHAPE = 2
@@ -32,6 +34,7 @@ TATN_OUT_FP32 = 1
 TATN_MASK_NONE = 0
 TATN_MASK_CAUSAL = 1
 TATN_MASK_KEY_PADDING = 2
+TATN_MASK_CUSTOM = 3
 
 # every symbol include/tatn_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (
@@ -73,6 +76,9 @@ class TatnAttnDesc(ctypes.Structure):
         ("visited_bitmap", ctypes.c_void_p),
         ("p_drop", ctypes.c_double),
         ("seed", ctypes.c_uint64),
+        ("custom_mask", ctypes.c_void_p),
+        ("custom_words", ctypes.c_int32),
+        ("custom_bstride", ctypes.c_int64),
     ]
 
 
@@ -110,6 +116,8 @@ def load() -> ctypes.CDLL:
     lib.tatn_strerror.restype = ctypes.c_char_p
     lib.tatn_abi_version.argtypes = []
     lib.tatn_abi_version.restype = ctypes.c_int
+    if lib.tatn_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH}: ABI version {lib.tatn_abi_version()} != {ABI_VERSION} (stale build?)")
     lib.tatn_last_launch_count.argtypes = []
     lib.tatn_last_launch_count.restype = ctypes.c_int
     if hasattr(lib, "tatn_debug_set_trace"):  # -DTATN_TRACE builds only

@@ -24,6 +24,7 @@ MASK_KINDS = {
     "none": _lib.TATN_MASK_NONE,
     "causal": _lib.TATN_MASK_CAUSAL,
     "key_padding": _lib.TATN_MASK_KEY_PADDING,
+    "custom": _lib.TATN_MASK_CUSTOM,
 }
 
 
@@ -53,6 +54,24 @@ class AttnSpec:
     out_fp32: bool = False  # write O / dQ / dK / dV in fp32 (no output rounding)
     p_drop: float = 0.0  # dropout probability in [0, 1) (reference's positional PRNG, dropout.cpp)
     seed: int = 0  # dropout seed; slice (b, h) uses seed + b*H + h
+    # mask="custom": bit-packed keep matrix from pack_custom_mask(), int32 [Nq, words] shared
+    # by every slice or [B, Nq, words] per batch element (MaskSpec::custom_additive)
+    custom: Optional[torch.Tensor] = None
+
+
+def pack_custom_mask(keep: torch.Tensor) -> torch.Tensor:
+    """Bit-pack a boolean keep matrix [..., Nq, Nk] (True = additive 0, False = -inf) into the
+    C ABI's custom_mask layout: int32 words [..., Nq, words], bit (j & 31) of word j >> 5,
+    words = ceil(Nk / 32) rounded up to a multiple of 4 (16-byte rows). Runs on keep's device."""
+    if keep.dtype != torch.bool:
+        keep = keep != 0
+    *lead, nq, nk = keep.shape
+    words = (nk + 127) // 128 * 4
+    padded = torch.zeros(*lead, nq, words * 32, dtype=torch.int64, device=keep.device)
+    padded[..., :nk] = keep.to(torch.int64)
+    bits = padded.view(*lead, nq, words, 32) << torch.arange(32, device=keep.device, dtype=torch.int64)
+    packed = bits.sum(-1)  # < 2^32
+    return torch.where(packed >= 2**31, packed - 2**32, packed).to(torch.int32).contiguous()
 
 
 def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttnDesc:
@@ -88,6 +107,17 @@ def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttn
     desc.visited_bitmap = spec.visited.data_ptr() if spec.visited is not None else None
     desc.p_drop = float(spec.p_drop)
     desc.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
+    if spec.mask == "custom":
+        cm = spec.custom
+        if cm is None or cm.dtype != torch.int32 or cm.dim() not in (2, 3) or cm.stride(-1) != 1:
+            raise ValueError("mask='custom' needs spec.custom = pack_custom_mask(keep) ([Nq, w] or [B, Nq, w] int32)")
+        if cm.shape[-2] != Nq or (cm.dim() == 3 and cm.shape[0] != B):
+            raise ValueError(f"custom mask shape {tuple(cm.shape)} does not match B={B}, Nq={Nq}")
+        desc.custom_mask = cm.data_ptr()
+        desc.custom_words = cm.shape[-1]
+        desc.custom_bstride = cm.stride(0) if cm.dim() == 3 else 0
+    else:
+        desc.custom_mask = None
     return desc
 
 

@@ -245,6 +245,33 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
   }
 }
 
+// ---------------------------------------------------------------- K2b (Custom masks only)
+// Transpose the keep bits [nb][Nq][words] (query rows) into [nb][Nk][Nq_pad/32] (key rows), so
+// K3's softmax thread (one key row) reads its 64 query bits of a Q tile with one 8-byte load.
+// One warp per 32 x 32 bit block: lane l loads row q0+l's word, 32 ballots transpose it.
+__global__ void __launch_bounds__(256) tatn_custom_transpose(const uint32_t* __restrict__ in, int words, int64_t bstride,
+                                                             int nb, int Nq, int Nk, int tw, uint32_t* __restrict__ out) {
+  const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const int kwords = (Nk + 31) / 32;
+  const long long total = static_cast<long long>(nb) * tw * kwords;
+  if (wid >= total) return;  // warp-uniform
+  const int kw = static_cast<int>(wid % kwords);
+  const long long r = wid / kwords;
+  const int qw = static_cast<int>(r % tw);
+  const int bsel = static_cast<int>(r / tw);
+  const int q = qw * 32 + lane;
+  const uint32_t w = (q < Nq) ? in[static_cast<size_t>(bsel) * bstride + static_cast<size_t>(q) * words + kw] : 0u;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t col = __ballot_sync(0xffffffffu, (w >> j) & 1u);  // bit l = keep(q0 + l, 32 kw + j)
+    if (lane == j) mine = col;
+  }
+  const int kj = kw * 32 + lane;
+  if (kj < Nk) out[(static_cast<size_t>(bsel) * Nk + kj) * tw + qw] = mine;
+}
+
 // ---------------------------------------------------------------- K3
 // Item w (one 128-key tile of one head) -> (bh, j). Items are laid out in head groups:
 // the key tiles of `group` heads are adjacent, so their Q / dO tiles and fp32 dQ
@@ -637,9 +664,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (r < kBwdQT) drop_rows[r] = drop_row_hash(p.drop_seed + static_cast<uint64_t>(it.bh), i0 + r);
           named_bar_sync(3 + sg, 128);
         }
-        const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0);
+        const bool custom_on = p.custom_t != nullptr;
+        const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0) || custom_on;
         // masked keys: kj >= kv_limit for every query; causal: kj > i0 + c  <=>  c < kj - i0
         const int c_lo = (kj >= sc.kv_limit) ? kBwdQT : (causal ? kj - i0 : 0);  // first visible query column
+        // Custom mask: keep bits of this key row for the tile's 64 queries (K2b's transpose)
+        uint2 cbits = make_uint2(~0u, ~0u);
+        if (custom_on) {
+          cbits = make_uint2(0u, 0u);
+          if (kj < p.Nk)
+            cbits = *reinterpret_cast<const uint2*>(
+                p.custom_t + (static_cast<size_t>(p.custom_t_b ? it.b : 0) * p.Nk + kj) * p.custom_t_words + i * 2);
+        }
         constexpr int kH0 = 0, kH1 = kSplit ? 1 : 2;  // halves (32 query columns) per warpgroup
         const int hbase = kSplit ? sg : 0;
         uint32_t sr[32], dp[32];
@@ -671,8 +707,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 p0 = ex2_approx(p0);
                 p1 = ex2_approx(p1);
                 if constexpr (kMasked) {
-                  p0 = (c < c_lo) ? 0.f : p0;
-                  p1 = (c + 1 < c_lo) ? 0.f : p1;
+                  const uint32_t cwv = (c < 32) ? cbits.x : cbits.y;
+                  p0 = (c < c_lo || ((cwv >> (c & 31)) & 1u) == 0u) ? 0.f : p0;
+                  p1 = (c + 1 < c_lo || ((cwv >> ((c + 1) & 31)) & 1u) == 0u) ? 0.f : p1;
                 }
                 const uint64_t nd = e ? d4.y : d4.x;
                 if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
@@ -912,6 +949,18 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   float* lse2 = dq_acc + rows * D;
   float* delta = lse2 + rows;
   int* item_counter = reinterpret_cast<int*>(delta + rows);
+  uint32_t* custom_t = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(item_counter) + 16);
+  const int custom_t_words = Nq_pad / 32;
+  const bool custom = d.mask_kind == TATN_MASK_CUSTOM;
+  if (custom) {
+    const int nb = d.custom_bstride != 0 ? d.B : 1;
+    const long long warps = static_cast<long long>(nb) * custom_t_words * ((d.Nk + 31) / 32);
+    const int blocks = static_cast<int>((warps * 32 + 255) / 256);
+    tatn_dev::tatn_custom_transpose<<<blocks, 256, 0, stream>>>(d.custom_mask, d.custom_words, d.custom_bstride, nb,
+                                                                 d.Nq, d.Nk, custom_t_words, custom_t);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   {
     const long long threads = static_cast<long long>(rows) * (D / 8);
     const int blocks = static_cast<int>((threads + 255) / 256);
@@ -948,6 +997,9 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.n_ktiles = p.tc;
   p.n_items = d.B * d.H * p.n_ktiles;
   p.item_counter = item_counter;
+  p.custom_t = custom ? custom_t : nullptr;
+  p.custom_t_words = custom_t_words;
+  p.custom_t_b = (custom && d.custom_bstride != 0) ? 1 : 0;
   p.group = tatn_host::schedule_group(d.B * d.H, p.n_ktiles, static_cast<double>(d.Nq) * D * 8.0, 1);
   p.dk_f32 = OUT_F32 ? static_cast<float*>(dk) : nullptr;
   p.dv_f32 = OUT_F32 ? static_cast<float*>(dv) : nullptr;
@@ -982,7 +1034,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  *launches = 3;
+  *launches = custom ? 4 : 3;
   return cudaSuccess;
 }
 

@@ -110,9 +110,17 @@ int validate(const tatn_attn_desc* d) {
   if (d->out_dtype != TATN_OUT_INPUT_DTYPE && d->out_dtype != TATN_OUT_FP32) return TATN_E_UNSUPPORTED;
   if (!(d->tau > 0.f) || !std::isfinite(d->tau)) return TATN_E_ARG;  // attn_config.cpp:52
   if (!(d->p_drop >= 0.0 && d->p_drop < 1.0)) return TATN_E_ARG;      // attn_config.cpp:54
-  if (d->mask_kind != TATN_MASK_NONE && d->mask_kind != TATN_MASK_CAUSAL && d->mask_kind != TATN_MASK_KEY_PADDING)
-    return TATN_E_UNSUPPORTED;
+  if (d->mask_kind != TATN_MASK_NONE && d->mask_kind != TATN_MASK_CAUSAL && d->mask_kind != TATN_MASK_KEY_PADDING &&
+      d->mask_kind != TATN_MASK_CUSTOM)
+    return TATN_E_ARG;  // not a tatn::MaskKind
   if (d->mask_kind == TATN_MASK_KEY_PADDING && d->valid_len == nullptr) return TATN_E_ARG;
+  if (d->mask_kind == TATN_MASK_CUSTOM) {
+    // custom mask must cover Nq x Nk (attn_config.cpp:50-52: "custom mask must be n x n")
+    if (d->custom_mask == nullptr) return TATN_E_ARG;
+    if (d->custom_words < (d->Nk + 31) / 32 || (d->custom_words % 4) != 0) return TATN_E_MASK;
+    if (d->custom_bstride != 0 && d->custom_bstride < static_cast<int64_t>(d->Nq) * d->custom_words) return TATN_E_MASK;
+    if ((reinterpret_cast<uintptr_t>(d->custom_mask) & 15u) != 0) return TATN_E_ARG;  // 16-byte row loads
+  }
   if (!strides_ok(d->q_str, d->H, d->Nq, d->d) || !strides_ok(d->k_str, d->H, d->Nk, d->d) ||
       !strides_ok(d->v_str, d->H, d->Nk, d->d) || !strides_ok(d->o_str, d->H, d->Nq, d->d))
     return TATN_E_SHAPE;
@@ -277,6 +285,9 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.o_sb = d.o_str[0];
   p.o_sh = d.o_str[1];
   p.o_sn = d.o_str[2];
+  p.custom = d.mask_kind == TATN_MASK_CUSTOM ? d.custom_mask : nullptr;
+  p.custom_words = d.custom_words;
+  p.custom_bstride = d.custom_bstride;
   const bool drop = d.p_drop > 0.0;
   set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
   const int sel = (d.d == 128 ? 8 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 4 : 0) + (f32 ? 2 : 0) + (drop ? 1 : 0);
@@ -314,7 +325,12 @@ size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc) {
   // dQ accumulator [B,H,Nq_pad,d] fp32 + lse2 [B,H,Nq_pad] + D [B,H,Nq_pad], Nq_pad = roundup(Nq, 128),
   // + the persistent backward's item counter
   const size_t rows = static_cast<size_t>(desc->B) * desc->H * ((desc->Nq + 127) / 128 * 128);
-  return rows * desc->d * sizeof(float) + 2 * rows * sizeof(float) + 16;  // + K3 item counter
+  size_t bytes = rows * desc->d * sizeof(float) + 2 * rows * sizeof(float) + 16;  // + K3 item counter
+  if (desc->mask_kind == TATN_MASK_CUSTOM) {  // + the custom mask transposed for K3 (K2b)
+    const size_t nb = desc->custom_bstride != 0 ? static_cast<size_t>(desc->B) : 1;
+    bytes += nb * static_cast<size_t>(desc->Nk) * ((desc->Nq + 127) / 128 * 4) * sizeof(uint32_t);
+  }
+  return bytes;
 }
 
 int tatn_bwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, const void* o, const void* dO,

@@ -447,6 +447,22 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     const float sl2 = p.scale_log2;
     const bool causal = p.mask_kind == kMaskCausal;
     const uint64_t sl2x2 = f2_pack(sl2, sl2);
+    // Custom mask (MaskKind::Custom): this row's keep bits, 4 words per 128-key tile. The row
+    // pointer is recomputed from the kernel parameters at each use (no live registers on the
+    // unmasked path).
+    const bool custom_on = p.custom != nullptr;
+    auto load_cw = [&](int t, uint32_t (&cw)[4]) {
+      if (p.custom != nullptr && grow < p.Nq) {
+        const uint4 w = *reinterpret_cast<const uint4*>(p.custom + static_cast<size_t>(b) * p.custom_bstride +
+                                                        static_cast<size_t>(grow) * p.custom_words + 4 * t);
+        cw[0] = w.x;
+        cw[1] = w.y;
+        cw[2] = w.z;
+        cw[3] = w.w;
+      } else {
+        cw[0] = cw[1] = cw[2] = cw[3] = (p.custom != nullptr) ? 0u : ~0u;  // rows past Nq are never stored
+      }
+    };
 
     float m_run = -INFINITY;  // running max of tau*s*log2(e), possibly stale by <= threshold
     float l_run = 0.f;        // running denominator relative to m_run
@@ -482,7 +498,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         tc_fence_before();
         mbar_arrive(BAR(kBarSFree));
         const int k0 = t * kBN;
-        const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0);
+        const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0) || custom_on;
         const int lim = min(sc.kv_limit, causal ? grow + 1 : sc.kv_limit) - k0;  // columns >= lim are masked
         auto step = [&](auto masked_t) {
           constexpr bool kMasked = decltype(masked_t)::value;
@@ -563,6 +579,15 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
           f2_unpack(rsum1, rs2, rs3);
           l_run += (rs0 + rs1) + (rs2 + rs3);
         };
+        if (custom_on) {  // Custom mask: -inf where the keep bit is 0 (then the usual masked step)
+          uint32_t cw[4];
+          load_cw(t, cw);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              sv[c][i] = ((cw[c] >> i) & 1u) ? sv[c][i] : __float_as_uint(-INFINITY);
+        }
         if (need_mask) step(std::true_type{});
         else step(std::false_type{});
         tmem_st_wait();
@@ -582,14 +607,17 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
       sph ^= 1;
       tc_fence_after();
       const int k0 = t * kBN;
-      const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0);
+      const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0) || custom_on;
+      uint32_t cw[4];
+      load_cw(t, cw);
       // masked scores -> -inf (diagonal / boundary tiles only)
       auto apply_mask = [&](uint32_t (&r)[32], int c) {
         if (need_mask) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int kj = k0 + c * 32 + i;
-            if ((kj >= sc.kv_limit) || (causal && kj > grow)) r[i] = __float_as_uint(-INFINITY);
+            if ((kj >= sc.kv_limit) || (causal && kj > grow) || ((cw[c] >> i) & 1u) == 0u)
+              r[i] = __float_as_uint(-INFINITY);
           }
         }
       };

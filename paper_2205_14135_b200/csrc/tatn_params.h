@@ -5,9 +5,8 @@
 
 namespace tatn_dev {
 
-// Mirrors tatn::MaskKind (reference attn_config.hpp:12) for the kinds the
-// device path implements. Custom (n x n additive) masks are not on the path.
-enum MaskKindDev : int { kMaskNone = 0, kMaskCausal = 1, kMaskKeyPadding = 2 };
+// Mirrors tatn::MaskKind (reference attn_config.hpp:12).
+enum MaskKindDev : int { kMaskNone = 0, kMaskCausal = 1, kMaskKeyPadding = 2, kMaskCustom = 3 };
 
 struct FwdParams {
   int B, H, Nq, Nk;
@@ -25,6 +24,9 @@ struct FwdParams {
   float drop_scale;          // 1 / (1 - p)
   float* o_f32;              // fp32 output mode: O written here directly (strides below)
   int64_t o_sb, o_sh, o_sn;
+  const uint32_t* custom;    // Custom mask: keep bits [Nq][custom_words] per batch element (or shared)
+  int custom_words;
+  int64_t custom_bstride;
 };
 
 struct BwdParams {
@@ -49,6 +51,9 @@ struct BwdParams {
   float* dk_f32;     // fp32 output mode: dK / dV written directly (strides below)
   float* dv_f32;
   int64_t k_sb, k_sh, k_sn, v_sb, v_sh, v_sn;
+  const uint32_t* custom_t;  // Custom mask transposed by K2b: keep bits [Bc][Nk][Nq_pad/32]
+  int custom_t_words;        // Nq_pad / 32
+  int custom_t_b;            // 1: one mask per batch element (b), 0: shared
 };
 
 }  // namespace tatn_dev

@@ -32,10 +32,13 @@ def empty_like_layout(t: torch.Tensor, dtype=None) -> torch.Tensor:
 
 
 def run_gpu(q, k, v, do, dtype, mask="none", valid_len=None, grid=None, backward=True, layout="bhnd",
-            visited=False, out_fp32=False, p_drop=0.0, seed=0):
-    """Forward (+ backward) on the device through the C ABI. Returns numpy fp64 outputs."""
+            visited=False, out_fp32=False, p_drop=0.0, seed=0, custom=None):
+    """Forward (+ backward) on the device through the C ABI. Returns numpy fp64 outputs.
+    custom: bool keep matrix [Nq, Nk] (shared) or [B, Nq, Nk] for mask="custom"."""
     qd, kd, vd = (to_dev(t, dtype, layout) for t in (q, k, v))
     spec = A.AttnSpec(mask=mask, out_fp32=out_fp32, p_drop=p_drop, seed=seed)
+    if custom is not None:
+        spec.custom = A.pack_custom_mask(torch.from_numpy(np.asarray(custom, dtype=bool)).cuda())
     if valid_len is not None:
         spec.valid_len = torch.as_tensor(np.asarray(valid_len, dtype=np.int32)).cuda()
     if grid is not None:
@@ -58,7 +61,7 @@ def run_gpu(q, k, v, do, dtype, mask="none", valid_len=None, grid=None, backward
         dod = to_dev(do, dtype, layout)
         dq, dk, dv = empty_like_layout(qd, odt), empty_like_layout(kd, odt), empty_like_layout(vd, odt)
         A.flash_bwd(qd, kd, vd, o, dod, lse, spec, dq=dq, dk=dk, dv=dv)
-        assert A.last_launch_count() == 3
+        assert A.last_launch_count() == (4 if mask == "custom" else 3)
         out.update(dq=dq.double().cpu().numpy(), dk=dk.double().cpu().numpy(), dv=dv.double().cpu().numpy())
     torch.cuda.synchronize()
     if visited:
@@ -94,12 +97,15 @@ def assert_close(name, got, ref, max_abs=MAX_ABS, rel_l2=REL_L2):
     return mx, rel
 
 
-def oracle_full(q, k, v, do, mask="none", valid_len=None, grid=None, backward=True, p_drop=0.0, seed=0):
-    o, lse = O.forward(q, k, v, mask=mask, valid_len=valid_len, grid=grid, p_drop=p_drop, seed=seed)
+def oracle_full(q, k, v, do, mask="none", valid_len=None, grid=None, backward=True, p_drop=0.0, seed=0, custom=None):
+    if custom is not None:  # [B, Nq, Nk] per batch element -> broadcast over heads
+        custom = np.asarray(custom, dtype=bool)
+        custom = custom[:, None] if custom.ndim == 3 else custom
+    o, lse = O.forward(q, k, v, mask=mask, valid_len=valid_len, grid=grid, p_drop=p_drop, seed=seed, custom=custom)
     out = {"o": o, "lse": lse}
     if backward:
         dq, dk, dv = O.backward(q, k, v, o, do, lse, mask=mask, valid_len=valid_len, grid=grid, p_drop=p_drop,
-                                seed=seed)
+                                seed=seed, custom=custom)
         out.update(dq=dq, dk=dk, dv=dv)
     return out
 

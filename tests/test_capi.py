@@ -40,7 +40,7 @@ def test_exports_have_c_linkage():
 
 def test_abi_version_and_strerror():
     lib = _lib.load()
-    assert lib.tatn_abi_version() == 2
+    assert lib.tatn_abi_version() == 3
     for code in range(7):
         assert _lib.strerror(code)
     assert _lib.strerror(99) == "unknown status"
@@ -82,7 +82,8 @@ def test_valid_descriptor_passes():
         (dict(tau=float("nan")), _lib.TATN_E_ARG),
         (dict(p_drop=1.0), _lib.TATN_E_ARG),  # p in [0, 1) (attn_config.cpp:54)
         (dict(p_drop=-0.1), _lib.TATN_E_ARG),
-        (dict(mask_kind=3), _lib.TATN_E_UNSUPPORTED),  # Custom n x n masks
+        (dict(mask_kind=3), _lib.TATN_E_ARG),  # Custom without its mask
+        (dict(mask_kind=9), _lib.TATN_E_ARG),  # not a MaskKind
         (dict(mask_kind=_lib.TATN_MASK_KEY_PADDING), _lib.TATN_E_ARG),  # no valid_len
     ],
 )
@@ -114,3 +115,24 @@ def test_workspace_formula():
     rows = 2 * 3 * 384  # Nq padded to a multiple of 128
     assert lib.tatn_bwd_workspace_bytes(ctypes.byref(d)) == rows * 64 * 4 + 2 * rows * 4 + 16
     assert lib.tatn_bwd_workspace_bytes(ctypes.byref(good_desc(B=0))) == 0
+
+
+def test_custom_mask_descriptor():
+    buf = (ctypes.c_uint32 * (300 * 12 + 4))()
+    base = (ctypes.addressof(buf) + 15) // 16 * 16
+    ok = good_desc(mask_kind=_lib.TATN_MASK_CUSTOM, custom_mask=base, custom_words=12)
+    assert validate(ok) == _lib.TATN_OK
+    # words must cover Nk (ceil(300/32) = 10, rounded to a multiple of 4 = 12) and be 16-byte multiples
+    assert validate(good_desc(mask_kind=3, custom_mask=base, custom_words=8)) == _lib.TATN_E_MASK
+    assert validate(good_desc(mask_kind=3, custom_mask=base, custom_words=10)) == _lib.TATN_E_MASK
+    assert validate(good_desc(mask_kind=3, custom_mask=base + 4, custom_words=12)) == _lib.TATN_E_ARG
+    # a per-batch stride smaller than one Nq x words mask overlaps
+    assert validate(good_desc(mask_kind=3, custom_mask=base, custom_words=12, custom_bstride=100)) == _lib.TATN_E_MASK
+    assert validate(good_desc(mask_kind=3, custom_mask=base, custom_words=12, custom_bstride=3600)) == _lib.TATN_OK
+    # the backward workspace adds the transposed mask [B or 1][Nk][Nq_pad/32]
+    lib = _lib.load()
+    rows = 2 * 3 * 384
+    base_ws = rows * 64 * 4 + 2 * rows * 4 + 16
+    assert lib.tatn_bwd_workspace_bytes(ctypes.byref(ok)) == base_ws + 300 * 12 * 4
+    per_b = good_desc(mask_kind=3, custom_mask=base, custom_words=12, custom_bstride=3600)
+    assert lib.tatn_bwd_workspace_bytes(ctypes.byref(per_b)) == base_ws + 2 * 300 * 12 * 4
