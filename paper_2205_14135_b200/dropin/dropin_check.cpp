@@ -126,6 +126,21 @@ int main() {
     check_dense({"n300_d64_padding0", 300, 300, 64, MaskSpec::key_padding(0)});
     check_dense({"n640_prefix400_d100_causal", 640, 400, 100, MaskSpec::causal()});
     check_dense({"n129_d16_none", 129, 129, 16, MaskSpec::none()});
+    // ---- Custom n x n additive masks (attn_config.hpp:27): random keep pattern with a
+    // fully masked row (O = 0, l = 0, m = -inf) and a key nobody attends to (dK = dV = 0)
+    {
+      const size_t n = 333;
+      Matrix pat(n, n);
+      uint64_t h = 0x9e3779b97f4a7c15ull;
+      for (size_t i = 0; i < n; ++i)
+        for (size_t j = 0; j < n; ++j) {
+          h ^= h << 13; h ^= h >> 7; h ^= h << 17;
+          const bool keep = (h % 10) < 6 && i != 7 && j != 11;
+          pat(i, j) = keep ? 0.0 : -std::numeric_limits<double>::infinity();
+        }
+      check_dense({"n333_d64_custom", n, n, 64, MaskSpec::custom_additive(pat)});
+      check_dense({"n333_prefix200_d128_custom", n, 200, 128, MaskSpec::custom_additive(pat)});
+    }
 
     // ---- counters equal the io_predict closed forms for uniform blocks
     {
@@ -269,8 +284,10 @@ int main() {
       drop.p_drop = 1.0;
       report("error_dropout_p_out_of_range", throws([&] { flash_forward(x, x, x, drop, plan, mem); }));
       AttnConfig cust = AttnConfig::make(n, d);
-      cust.mask = MaskSpec::custom_additive(Matrix(n, n));
-      report("error_custom_mask_unsupported", throws([&] { flash_forward(x, x, x, cust, plan, mem); }));
+      cust.mask = MaskSpec::custom_additive(Matrix::filled(n, n, 1.0));  // entries must be 0 or -inf
+      report("error_custom_mask_entries", throws([&] { flash_forward(x, x, x, cust, plan, mem); }));
+      cust.mask = MaskSpec::custom_additive(Matrix(n - 1, n - 1));  // must be n x n
+      report("error_custom_mask_shape", throws([&] { flash_forward(x, x, x, cust, plan, mem); }));
       AttnConfig ok = AttnConfig::make(n, d);
       const TilePlan wrong = plan_tiles(2 * n, d, 65536);
       report("error_plan_mismatch", throws([&] { flash_forward(x, x, x, ok, wrong, mem); }));

@@ -17,8 +17,9 @@
 // Dropout follows the reference's positional generator bit for bit (the mask at
 // (i, j) is a pure function of (seed, i, j), dropout.hpp:14-30), so forward and
 // backward regenerate identical masks. There is no CPU fallback: unsupported
-// inputs (Custom n x n masks, d > 128, block sizes that are not multiples of
-// 128) throw, and a missing sm_100 device surfaces as std::runtime_error.
+// inputs (d > 128, block sizes that are not multiples of 128) throw, and a missing
+// sm_100 device surfaces as std::runtime_error. Custom n x n masks are bit-packed
+// into the ABI's keep matrix.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -145,8 +146,6 @@ void check_inputs(const char* op, const Matrix& q, const Matrix& k, const Matrix
   if (k.rows() != v.rows()) throw std::invalid_argument(std::string(op) + ": K and V row counts differ");
   if (k.rows() > cfg.n || k.rows() < 1) throw std::invalid_argument(std::string(op) + ": bad key count");
   if (has_nan(q) || has_nan(k) || has_nan(v)) throw std::invalid_argument(std::string(op) + ": NaN input");
-  if (cfg.mask.kind == MaskKind::Custom)
-    throw std::invalid_argument(std::string(op) + ": Custom n x n masks are not supported on the sm_100a path");
 }
 
 void check_plan(const char* op, const TilePlan& plan, std::size_t n, std::size_t d) {
@@ -177,8 +176,9 @@ Problem make_problem(const Matrix& q, const Matrix& k, const AttnConfig& cfg) {
   d.k_str[0] = sk; d.k_str[1] = sk; d.k_str[2] = P.dp;
   d.v_str[0] = sk; d.v_str[1] = sk; d.v_str[2] = P.dp;
   d.tau = static_cast<float>(cfg.tau);
-  d.mask_kind = cfg.mask.kind == MaskKind::Causal ? TATN_MASK_CAUSAL
+  d.mask_kind = cfg.mask.kind == MaskKind::Causal       ? TATN_MASK_CAUSAL
                 : cfg.mask.kind == MaskKind::KeyPadding ? TATN_MASK_KEY_PADDING
+                : cfg.mask.kind == MaskKind::Custom     ? TATN_MASK_CUSTOM
                                                         : TATN_MASK_NONE;
   d.tr = static_cast<int32_t>((P.n + 127) / 128);
   d.tc = static_cast<int32_t>((P.nk + 127) / 128);
@@ -186,6 +186,30 @@ Problem make_problem(const Matrix& q, const Matrix& k, const AttnConfig& cfg) {
   d.seed = cfg.seed;
   return P;
 }
+
+// MaskKind::Custom: the n x n additive pattern (0 keep / -inf mask, validated by
+// AttnConfig::validate) bit-packed into the ABI's keep matrix [n][words], words =
+// ceil(nk / 128) * 4, and uploaded; the descriptor points at it for the call's lifetime.
+struct CustomMask {
+  DevBuf buf;
+  int32_t words;
+  CustomMask(const AttnConfig& cfg, std::size_t n, std::size_t nk)
+      : buf(cfg.mask.kind == MaskKind::Custom ? n * ((nk + 127) / 128 * 4) * 4 : 0),
+        words(static_cast<int32_t>((nk + 127) / 128 * 4)) {
+    if (cfg.mask.kind != MaskKind::Custom) return;
+    std::vector<uint32_t> bits(n * static_cast<std::size_t>(words), 0u);
+    for (std::size_t i = 0; i < n; ++i)
+      for (std::size_t j = 0; j < nk; ++j)
+        if (cfg.mask.custom(i, j) == 0.0) bits[i * words + j / 32] |= 1u << (j % 32);
+    check_cuda(cudaMemcpy(buf.p, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice), "upload custom mask");
+  }
+  void attach(tatn_attn_desc& d) const {
+    if (d.mask_kind != TATN_MASK_CUSTOM) return;
+    d.custom_mask = static_cast<const uint32_t*>(buf.p);
+    d.custom_words = words;
+    d.custom_bstride = 0;
+  }
+};
 
 // Expand a BlockMask whose block sizes are multiples of 128 to the kernels' 128 x 128 tile grid.
 std::vector<uint8_t> tile_grid(const BlockMask& bm, std::size_t n, std::size_t nk) {
@@ -269,6 +293,8 @@ FlashSaved forward_impl(const char* op, const Matrix& q, const Matrix& k, const 
     check_cuda(cudaMemcpy(dvl.p, &vl, 4, cudaMemcpyHostToDevice), "upload valid_len");
     P.desc.valid_len = static_cast<const int32_t*>(dvl.p);
   }
+  const CustomMask cmask(cfg, P.n, P.nk);
+  cmask.attach(P.desc);
   std::vector<uint8_t> grid;
   DevBuf dgrid(bm ? ((P.n + 127) / 128) * ((P.nk + 127) / 128) : 0);
   if (bm) {
@@ -364,6 +390,8 @@ Gradients backward_impl(const char* op, const FlashSaved& saved, const Matrix& q
     check_cuda(cudaMemcpy(dvl.p, &vl, 4, cudaMemcpyHostToDevice), "upload valid_len");
     P.desc.valid_len = static_cast<const int32_t*>(dvl.p);
   }
+  const CustomMask cmask(cfg, P.n, P.nk);
+  cmask.attach(P.desc);
   DevBuf dgrid(bm ? ((P.n + 127) / 128) * ((P.nk + 127) / 128) : 0);
   if (bm) {
     const auto grid = tile_grid(*bm, P.n, P.nk);
