@@ -43,7 +43,8 @@ typedef enum {
   TATN_E_WORKSPACE = 6     /* workspace too small                                                */
 } tatn_status;
 
-typedef enum { TATN_DTYPE_BF16 = 0, TATN_DTYPE_FP16 = 1 } tatn_dtype;
+/* TATN_DTYPE_FP32 is an output type of tatn_merge_partials only. */
+typedef enum { TATN_DTYPE_BF16 = 0, TATN_DTYPE_FP16 = 1, TATN_DTYPE_FP32 = 2 } tatn_dtype;
 
 /* Output precision: O (forward) and dQ/dK/dV (backward) are written either in
  * the 16-bit input dtype or in fp32 (the "fp32 check mode" — no output
@@ -95,7 +96,23 @@ typedef struct {
   const uint32_t* custom_mask;
   int32_t custom_words;
   int64_t custom_bstride;
+  /* Sequence-parallel key shard (ABI v3): key j of this call is global key
+   * k_offset + j of an Nq-long sequence, for the causal / key-padding / custom predicates and
+   * the dropout hash. 0 for ordinary calls; else a multiple of 128 with k_offset + Nk <= Nq and
+   * no block grid. Partial (o, lse) pairs of the shards combine with tatn_merge_partials. */
+  int32_t k_offset;
 } tatn_attn_desc;
+
+/* Merge R partial attention results over disjoint key shards (merge_stats, softmax.hpp:48-59,
+ * softmax.cpp:62-83, in log form): per row m = max_r lse_r, w_r = exp(lse_r - m),
+ * o = sum_r w_r o_r / sum_r w_r, lse = m + ln(sum_r w_r); rows with every lse_r = -inf give
+ * o = 0, lse = -inf. o_parts: fp32 [R][B][H][Nq][d] contiguous (each shard's tatn_fwd output in
+ * TATN_OUT_FP32 mode); lse_parts: fp32 [R][B][H][Nq]. o: o_dtype with element strides o_str of
+ * b, h, n (d contiguous); lse: fp32 [B][H][Nq]. The exchange that brings the partials together
+ * (NCCL all-gather) is the caller's. */
+int tatn_merge_partials(int32_t R, int32_t B, int32_t H, int32_t Nq, int32_t d, const float* o_parts,
+                        const float* lse_parts, void* o, int32_t o_dtype, const int64_t o_str[3], float* lse,
+                        void* stream);
 
 /* Host-only descriptor check (no device access); same codes as the compute calls. */
 int tatn_validate(const tatn_attn_desc* desc);

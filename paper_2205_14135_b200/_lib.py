@@ -27,6 +27,7 @@ TATN_E_WORKSPACE = 6
 
 TATN_DTYPE_BF16 = 0
 TATN_DTYPE_FP16 = 1
+TATN_DTYPE_FP32 = 2  # tatn_merge_partials output only
 
 TATN_OUT_INPUT_DTYPE = 0
 TATN_OUT_FP32 = 1
@@ -47,6 +48,7 @@ EXPORTED_SYMBOLS = (
     "tatn_last_launch_count",
     "tatn_profile_enable",
     "tatn_profile_read",
+    "tatn_merge_partials",
 )
 
 
@@ -79,6 +81,7 @@ class TatnAttnDesc(ctypes.Structure):
         ("custom_mask", ctypes.c_void_p),
         ("custom_words", ctypes.c_int32),
         ("custom_bstride", ctypes.c_int64),
+        ("k_offset", ctypes.c_int32),
     ]
 
 
@@ -127,6 +130,9 @@ def load() -> ctypes.CDLL:
     lib.tatn_profile_enable.restype = ctypes.c_int
     lib.tatn_profile_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
     lib.tatn_profile_read.restype = ctypes.c_int
+    i32 = ctypes.c_int32
+    lib.tatn_merge_partials.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, i32, ctypes.POINTER(ctypes.c_int64), vp, vp]
+    lib.tatn_merge_partials.restype = ctypes.c_int
     _lib = lib
     return lib
 

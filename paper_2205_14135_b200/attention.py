@@ -54,6 +54,7 @@ class AttnSpec:
     out_fp32: bool = False  # write O / dQ / dK / dV in fp32 (no output rounding)
     p_drop: float = 0.0  # dropout probability in [0, 1) (reference's positional PRNG, dropout.cpp)
     seed: int = 0  # dropout seed; slice (b, h) uses seed + b*H + h
+    k_offset: int = 0  # key shard: key j is global key k_offset + j (sequence parallel; multiple of 128)
     # mask="custom": bit-packed keep matrix from pack_custom_mask(), int32 [Nq, words] shared
     # by every slice or [B, Nq, words] per batch element (MaskSpec::custom_additive)
     custom: Optional[torch.Tensor] = None
@@ -107,6 +108,7 @@ def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttn
     desc.visited_bitmap = spec.visited.data_ptr() if spec.visited is not None else None
     desc.p_drop = float(spec.p_drop)
     desc.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
+    desc.k_offset = int(spec.k_offset)
     if spec.mask == "custom":
         cm = spec.custom
         if cm is None or cm.dtype != torch.int32 or cm.dim() not in (2, 3) or cm.stride(-1) != 1:
@@ -187,3 +189,30 @@ def flash_bwd(q, k, v, o, dO, lse, spec: Optional[AttnSpec] = None, dq=None, dk=
 
 def last_launch_count() -> int:
     return _lib.load().tatn_last_launch_count()
+
+
+def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor, out: Optional[torch.Tensor] = None,
+                   lse: Optional[torch.Tensor] = None, stream=None):
+    """Combine R partial (O_r, LSE_r) over disjoint key shards into (O, LSE) with the
+    reference's merge_stats algebra (softmax.cpp:62-83), on the device (tatn_merge_partials).
+    o_parts: fp32 [R, B, H, Nq, d] contiguous; lse_parts: fp32 [R, B, H, Nq]. out: fp32 /
+    bf16 / fp16 [B, H, Nq, d] (default fp32)."""
+    lib = _lib.load()
+    if o_parts.dtype != torch.float32 or lse_parts.dtype != torch.float32:
+        raise TypeError("partials must be fp32 (tatn_fwd with out_fp32=True)")
+    if not (o_parts.is_contiguous() and lse_parts.is_contiguous()):
+        raise ValueError("partials must be contiguous [R, B, H, Nq, d] / [R, B, H, Nq]")
+    R, B, H, Nq, d = o_parts.shape
+    if tuple(lse_parts.shape) != (R, B, H, Nq):
+        raise ValueError(f"lse_parts shape {tuple(lse_parts.shape)} != {(R, B, H, Nq)}")
+    if out is None:
+        out = torch.empty((B, H, Nq, d), dtype=torch.float32, device=o_parts.device)
+    if lse is None:
+        lse = torch.empty((B, H, Nq), dtype=torch.float32, device=o_parts.device)
+    code = {torch.bfloat16: _lib.TATN_DTYPE_BF16, torch.float16: _lib.TATN_DTYPE_FP16,
+            torch.float32: _lib.TATN_DTYPE_FP32}[out.dtype]
+    st = (ctypes.c_int64 * 3)(*_strides(out, "out"))
+    s = stream if stream is not None else torch.cuda.current_stream(o_parts.device).cuda_stream
+    _check(lib.tatn_merge_partials(R, B, H, Nq, d, o_parts.data_ptr(), lse_parts.data_ptr(), out.data_ptr(), code,
+                                   st, lse.data_ptr(), ctypes.c_void_p(s)), "tatn_merge_partials")
+    return out, lse

@@ -128,7 +128,8 @@ __device__ __forceinline__ BwdSched make_bwd_sched(const BwdParams& p, int b, in
   BwdSched s;
   s.k0 = j * kBwdKT;
   int kv_limit = p.Nk;
-  if (p.mask_kind == kMaskKeyPadding && p.valid_len != nullptr) kv_limit = min(kv_limit, max(p.valid_len[b], 0));
+  // key j of this call is global key k_off + j (sequence-parallel shards); valid_len is global
+  if (p.mask_kind == kMaskKeyPadding && p.valid_len != nullptr) kv_limit = min(kv_limit, max(p.valid_len[b] - p.k_off, 0));
   s.kv_limit = kv_limit;
   s.tc = p.tc;
   const int n_qt = (p.Nq + kBwdQT - 1) / kBwdQT;
@@ -138,7 +139,7 @@ __device__ __forceinline__ BwdSched make_bwd_sched(const BwdParams& p, int b, in
     s.i_end = n_qt;
   } else {
     s.gcol = nullptr;
-    s.i_begin = (p.mask_kind == kMaskCausal) ? (s.k0 / kBwdQT) : 0;
+    s.i_begin = (p.mask_kind == kMaskCausal) ? ((s.k0 + p.k_off) / kBwdQT) : 0;
     s.i_end = (s.k0 < kv_limit) ? n_qt : 0;
   }
   if (s.i_begin > s.i_end) s.i_begin = s.i_end;
@@ -250,7 +251,8 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
 // K3's softmax thread (one key row) reads its 64 query bits of a Q tile with one 8-byte load.
 // One warp per 32 x 32 bit block: lane l loads row q0+l's word, 32 ballots transpose it.
 __global__ void __launch_bounds__(256) tatn_custom_transpose(const uint32_t* __restrict__ in, int words, int64_t bstride,
-                                                             int nb, int Nq, int Nk, int tw, uint32_t* __restrict__ out) {
+                                                             int nb, int Nq, int Nk, int tw, uint32_t* __restrict__ out,
+                                                             int kw_off) {
   const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = static_cast<int>(threadIdx.x & 31);
   const int kwords = (Nk + 31) / 32;
@@ -261,7 +263,8 @@ __global__ void __launch_bounds__(256) tatn_custom_transpose(const uint32_t* __r
   const int qw = static_cast<int>(r % tw);
   const int bsel = static_cast<int>(r / tw);
   const int q = qw * 32 + lane;
-  const uint32_t w = (q < Nq) ? in[static_cast<size_t>(bsel) * bstride + static_cast<size_t>(q) * words + kw] : 0u;
+  const uint32_t w =
+      (q < Nq) ? in[static_cast<size_t>(bsel) * bstride + static_cast<size_t>(q) * words + kw_off + kw] : 0u;
   uint32_t mine = 0;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
@@ -665,9 +668,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           named_bar_sync(3 + sg, 128);
         }
         const bool custom_on = p.custom_t != nullptr;
-        const bool need_mask = (sc.k0 + kBwdKT > sc.kv_limit) || (causal && sc.k0 + kBwdKT - 1 > i0) || custom_on;
-        // masked keys: kj >= kv_limit for every query; causal: kj > i0 + c  <=>  c < kj - i0
-        const int c_lo = (kj >= sc.kv_limit) ? kBwdQT : (causal ? kj - i0 : 0);  // first visible query column
+        const bool need_mask =
+            (sc.k0 + kBwdKT > sc.kv_limit) || (causal && p.k_off + sc.k0 + kBwdKT - 1 > i0) || custom_on;
+        // masked keys: kj >= kv_limit for every query; causal: k_off + kj > i0 + c  <=>  c < k_off + kj - i0
+        const int c_lo = (kj >= sc.kv_limit) ? kBwdQT : (causal ? p.k_off + kj - i0 : 0);  // first visible query
         // Custom mask: keep bits of this key row for the tile's 64 queries (K2b's transpose)
         uint2 cbits = make_uint2(~0u, ~0u);
         if (custom_on) {
@@ -715,8 +719,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
                   float d0, d1;
                   f2_unpack(nd, d0, d1);
-                  const float z0 = drop_keep(drop_rows[c], kj, p.drop_thresh) ? p.drop_scale : 0.f;
-                  const float z1 = drop_keep(drop_rows[c + 1], kj, p.drop_thresh) ? p.drop_scale : 0.f;
+                  const float z0 = drop_keep(drop_rows[c], p.k_off + kj, p.drop_thresh) ? p.drop_scale : 0.f;
+                  const float z1 = drop_keep(drop_rows[c + 1], p.k_off + kj, p.drop_thresh) ? p.drop_scale : 0.f;
                   dk[k] = pack2<BF16>(p0 * fmaf(__uint_as_float(dp[2 * k]), z0, d0),
                                       p1 * fmaf(__uint_as_float(dp[2 * k + 1]), z1, d1));
                   pk[k] = pack2<BF16>(p0 * z0, p1 * z1);
@@ -957,7 +961,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     const long long warps = static_cast<long long>(nb) * custom_t_words * ((d.Nk + 31) / 32);
     const int blocks = static_cast<int>((warps * 32 + 255) / 256);
     tatn_dev::tatn_custom_transpose<<<blocks, 256, 0, stream>>>(d.custom_mask, d.custom_words, d.custom_bstride, nb,
-                                                                 d.Nq, d.Nk, custom_t_words, custom_t);
+                                                                 d.Nq, d.Nk, custom_t_words, custom_t, d.k_offset / 32);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1000,6 +1004,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.custom_t = custom ? custom_t : nullptr;
   p.custom_t_words = custom_t_words;
   p.custom_t_b = (custom && d.custom_bstride != 0) ? 1 : 0;
+  p.k_off = d.k_offset;
   p.group = tatn_host::schedule_group(d.B * d.H, p.n_ktiles, static_cast<double>(d.Nq) * D * 8.0, 1);
   p.dk_f32 = OUT_F32 ? static_cast<float*>(dk) : nullptr;
   p.dv_f32 = OUT_F32 ? static_cast<float*>(dv) : nullptr;

@@ -131,6 +131,10 @@ int validate(const tatn_attn_desc* d) {
     if (tc > 2048 || 2 * tr > 4096) return TATN_E_UNSUPPORTED;  // block-sparse bitmask capacity (N <= 256K)
   }
   if (d->visited_bitmap != nullptr && (d->tr != tr || d->tc != tc)) return TATN_E_MASK;
+  // sequence-parallel key shard: keys are global keys [k_offset, k_offset + Nk) of an Nq-long sequence
+  if (d->k_offset < 0 || (d->k_offset % 128) != 0 || static_cast<int64_t>(d->k_offset) + d->Nk > d->Nq)
+    return TATN_E_SHAPE;
+  if (d->k_offset != 0 && d->block_grid != nullptr) return TATN_E_UNSUPPORTED;
   if (d->Nq > (1 << 24) || static_cast<int64_t>(d->B) * d->H * ((d->Nq + 127) / 128) > (1ll << 31) - 1)
     return TATN_E_SHAPE;
   return TATN_OK;
@@ -196,6 +200,25 @@ extern "C" {
 int tatn_validate(const tatn_attn_desc* desc) { return validate(desc); }
 
 int tatn_abi_version(void) { return TATN_B200_ABI_VERSION; }
+
+int tatn_merge_partials(int32_t R, int32_t B, int32_t H, int32_t Nq, int32_t d, const float* o_parts,
+                        const float* lse_parts, void* o, int32_t o_dtype, const int64_t o_str[3], float* lse,
+                        void* stream) {
+  g_last_launches = 0;
+  if (R < 1 || B < 1 || H < 1 || Nq < 1 || (d != 64 && d != 128)) return TATN_E_SHAPE;
+  if (!o_parts || !lse_parts || !o || !lse || !o_str) return TATN_E_ARG;
+  if (o_dtype != TATN_DTYPE_BF16 && o_dtype != TATN_DTYPE_FP16 && o_dtype != TATN_DTYPE_FP32) return TATN_E_ARG;
+  for (int i = 0; i < 3; ++i)
+    if (o_str[i] <= 0 || (o_str[i] % 8) != 0) return TATN_E_SHAPE;
+  const long long rows = static_cast<long long>(B) * H * Nq;
+  const long long threads = rows * (d / 8);
+  const int blocks = static_cast<int>((threads + 255) / 256);
+  tatn_dev::tatn_merge_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      R, rows, d, H, Nq, o_parts, lse_parts, o, o_dtype, o_str[0], o_str[1], o_str[2], lse);
+  if (cudaGetLastError() != cudaSuccess) return TATN_E_CUDA;
+  g_last_launches = 1;
+  return TATN_OK;
+}
 
 int tatn_last_launch_count(void) { return g_last_launches; }
 
@@ -288,6 +311,7 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.custom = d.mask_kind == TATN_MASK_CUSTOM ? d.custom_mask : nullptr;
   p.custom_words = d.custom_words;
   p.custom_bstride = d.custom_bstride;
+  p.k_off = d.k_offset;
   const bool drop = d.p_drop > 0.0;
   set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
   const int sel = (d.d == 128 ? 8 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 4 : 0) + (f32 ? 2 : 0) + (drop ? 1 : 0);

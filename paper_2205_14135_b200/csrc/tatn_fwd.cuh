@@ -102,7 +102,8 @@ __device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, in
   FwdSched s;
   s.sparse = p.grid != nullptr;
   int kv_limit = p.Nk;
-  if (p.mask_kind == kMaskKeyPadding && p.valid_len != nullptr) kv_limit = min(kv_limit, max(p.valid_len[b], 0));
+  // key j of this call is global key k_off + j (sequence-parallel shards); valid_len is global
+  if (p.mask_kind == kMaskKeyPadding && p.valid_len != nullptr) kv_limit = min(kv_limit, max(p.valid_len[b] - p.k_off, 0));
   s.kv_limit = kv_limit;
   const int ntiles_kv = (kv_limit + kBN - 1) / kBN;
   s.T = 0;
@@ -117,7 +118,10 @@ __device__ __forceinline__ FwdSched make_fwd_sched(const FwdParams& p, int b, in
         s.row[q] = (qt < p.tr) ? p.grid + static_cast<size_t>(qt) * p.tc : nullptr;
       } else {
         n = ntiles_kv;
-        if (p.mask_kind == kMaskCausal) n = min(n, (s.q0[q] + kBM - 1) / kBN + 1);
+        if (p.mask_kind == kMaskCausal) {  // last visible global key of the tile: q0 + 127
+          const int last = s.q0[q] + kBM - 1 - p.k_off;
+          n = min(n, last >= 0 ? last / kBN + 1 : 0);
+        }
       }
     }
     s.nkv[q] = n;
@@ -447,6 +451,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     const float sl2 = p.scale_log2;
     const bool causal = p.mask_kind == kMaskCausal;
     const uint64_t sl2x2 = f2_pack(sl2, sl2);
+    const int my_q0c = my_q0 - p.k_off, growc = grow - p.k_off;  // query rows in local key coordinates
     // Custom mask (MaskKind::Custom): this row's keep bits, 4 words per 128-key tile. The row
     // pointer is recomputed from the kernel parameters at each use (no live registers on the
     // unmasked path).
@@ -454,7 +459,8 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     auto load_cw = [&](int t, uint32_t (&cw)[4]) {
       if (p.custom != nullptr && grow < p.Nq) {
         const uint4 w = *reinterpret_cast<const uint4*>(p.custom + static_cast<size_t>(b) * p.custom_bstride +
-                                                        static_cast<size_t>(grow) * p.custom_words + 4 * t);
+                                                        static_cast<size_t>(grow) * p.custom_words + p.k_off / 32 +
+                                                        4 * t);
         cw[0] = w.x;
         cw[1] = w.y;
         cw[2] = w.z;
@@ -498,8 +504,8 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         tc_fence_before();
         mbar_arrive(BAR(kBarSFree));
         const int k0 = t * kBN;
-        const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0) || custom_on;
-        const int lim = min(sc.kv_limit, causal ? grow + 1 : sc.kv_limit) - k0;  // columns >= lim are masked
+        const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0c) || custom_on;
+        const int lim = min(sc.kv_limit, causal ? growc + 1 : sc.kv_limit) - k0;  // columns >= lim are masked
         auto step = [&](auto masked_t) {
           constexpr bool kMasked = decltype(masked_t)::value;
           if constexpr (kMasked) {
@@ -563,7 +569,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
               float p0, p1;
               f2_unpack(pv, p0, p1);
               if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
-                const int j0 = k0 + c * 32 + 2 * k;
+                const int j0 = p.k_off + k0 + c * 32 + 2 * k;  // global key index
                 p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
                 p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
               }
@@ -607,7 +613,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
       sph ^= 1;
       tc_fence_after();
       const int k0 = t * kBN;
-      const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0) || custom_on;
+      const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0c) || custom_on;
       uint32_t cw[4];
       load_cw(t, cw);
       // masked scores -> -inf (diagonal / boundary tiles only)
@@ -616,7 +622,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int kj = k0 + c * 32 + i;
-            if ((kj >= sc.kv_limit) || (causal && kj > grow) || ((cw[c] >> i) & 1u) == 0u)
+            if ((kj >= sc.kv_limit) || (causal && kj > growc) || ((cw[c] >> i) & 1u) == 0u)
               r[i] = __float_as_uint(-INFINITY);
           }
         }
@@ -672,7 +678,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
                 float p0, p1;
                 f2_unpack(pv, p0, p1);
                 if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
-                  const int j0 = k0 + c * 32 + 2 * k;
+                  const int j0 = p.k_off + k0 + c * 32 + 2 * k;  // global key index
                   p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
                   p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
                 }
@@ -854,4 +860,58 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
   }
 }
 
+}  // namespace tatn_dev
+
+namespace tatn_dev {
+// ---------------------------------------------------------------- partial-result merge
+// merge_stats (softmax.cpp:62-83) in log form over R key shards; one thread per 8 elements
+// of a row. HBM-bound: reads R * (d * 4 + 4) bytes and writes d * es + 4 bytes per row.
+__global__ void __launch_bounds__(256) tatn_merge_kernel(int R, long long rows, int d, int H, int Nq,
+                                                         const float* __restrict__ o_parts,
+                                                         const float* __restrict__ lse_parts, void* __restrict__ o,
+                                                         int o_dtype, int64_t ob, int64_t oh, int64_t on,
+                                                         float* __restrict__ lse) {
+  const int chunks = d / 8;
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long row = gid / chunks;
+  const int c = static_cast<int>(gid - row * chunks);
+  if (row >= rows) return;
+  float m = -INFINITY;
+  for (int r = 0; r < R; ++r) m = fmaxf(m, lse_parts[static_cast<size_t>(r) * rows + row]);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float wsum = 0.f;
+  if (m != -INFINITY) {
+    for (int r = 0; r < R; ++r) {
+      const float lr = lse_parts[static_cast<size_t>(r) * rows + row];
+      const float w = (lr == -INFINITY) ? 0.f : expf(lr - m);
+      if (w == 0.f) continue;
+      wsum += w;
+      const float4* src = reinterpret_cast<const float4*>(o_parts + (static_cast<size_t>(r) * rows + row) * d + c * 8);
+      const float4 a = src[0], b = src[1];
+      acc[0] = fmaf(w, a.x, acc[0]); acc[1] = fmaf(w, a.y, acc[1]); acc[2] = fmaf(w, a.z, acc[2]);
+      acc[3] = fmaf(w, a.w, acc[3]); acc[4] = fmaf(w, b.x, acc[4]); acc[5] = fmaf(w, b.y, acc[5]);
+      acc[6] = fmaf(w, b.z, acc[6]); acc[7] = fmaf(w, b.w, acc[7]);
+    }
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  const long long bh = row / Nq;
+  const int n = static_cast<int>(row - bh * Nq);
+  const size_t off = static_cast<size_t>(bh / H) * ob + static_cast<size_t>(bh % H) * oh + static_cast<size_t>(n) * on + c * 8;
+  if (o_dtype == 2) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(o) + off);
+    dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+  } else {
+    uint4 out;
+    if (o_dtype == 0) {
+      out = make_uint4(pack2<true>(acc[0] * inv, acc[1] * inv), pack2<true>(acc[2] * inv, acc[3] * inv),
+                       pack2<true>(acc[4] * inv, acc[5] * inv), pack2<true>(acc[6] * inv, acc[7] * inv));
+    } else {
+      out = make_uint4(pack2<false>(acc[0] * inv, acc[1] * inv), pack2<false>(acc[2] * inv, acc[3] * inv),
+                       pack2<false>(acc[4] * inv, acc[5] * inv), pack2<false>(acc[6] * inv, acc[7] * inv));
+    }
+    *reinterpret_cast<uint4*>(static_cast<uint16_t*>(o) + off) = out;
+  }
+  if (c == 0) lse[row] = wsum > 0.f ? m + logf(wsum) : -INFINITY;
+}
 }  // namespace tatn_dev

@@ -27,6 +27,7 @@ struct FwdParams {
   const uint32_t* custom;    // Custom mask: keep bits [Nq][custom_words] per batch element (or shared)
   int custom_words;
   int64_t custom_bstride;
+  int k_off;                 // global index of key 0 (sequence-parallel key shards; multiple of 128)
 };
 
 struct BwdParams {
@@ -54,6 +55,7 @@ struct BwdParams {
   const uint32_t* custom_t;  // Custom mask transposed by K2b: keep bits [Bc][Nk][Nq_pad/32]
   int custom_t_words;        // Nq_pad / 32
   int custom_t_b;            // 1: one mask per batch element (b), 0: shared
+  int k_off;                 // global index of key 0 (sequence-parallel key shards; multiple of 128)
 };
 
 }  // namespace tatn_dev
