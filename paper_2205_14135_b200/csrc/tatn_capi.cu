@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -19,16 +20,35 @@
 #include "../../include/tatn_b200.h"
 #include "tatn_bwd.cuh"
 #include "tatn_fwd.cuh"
+#include "tatn_fwd1.cuh"
 
 namespace tatn_host {
 int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm = 1);
+int sm_count();
 }  // namespace tatn_host
 using tatn_host::set_dropout;
 using tatn_host::schedule_group;
 
+// Self-resetting item counters of the persistent d = 64 forward ({next, finished CTAs} per slot),
+// handed out round-robin per launch so concurrent launches on different streams do not share one.
+__device__ int g_tatn_fwd_ctr[2 * 64];
+
 namespace {
 
 thread_local int g_last_launches = 0;
+
+int* fwd_counter() {
+  static std::atomic<unsigned> rr{0};
+  static int* base[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (base[dev] == nullptr) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_tatn_fwd_ctr) != cudaSuccess) return nullptr;
+    base[dev] = static_cast<int*>(p);
+  }
+  return base[dev] + 2 * (rr.fetch_add(1) % 64);
+}
 
 // ---- optional event timing of the main kernels (tatn_profile_*)
 struct Profiler {
@@ -147,11 +167,14 @@ CUtensorMapDataType tma_dtype(int dtype) {
 #ifndef TATN_FWD_NQ_D64
 #define TATN_FWD_NQ_D64 1  // d = 64: one Q tile per CTA, two CTAs per SM
 #endif
-template <int D, bool BF16, bool OUT_F32, bool DROP, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
-cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
-                       const tatn_dev::FwdParams& p, cudaStream_t stream) {
-  using Cfg = tatn_dev::FwdCfg<D, NQ>;
-  auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ, DROP>;
+#ifndef TATN_FWD_PERSISTENT
+#define TATN_FWD_PERSISTENT 1  // d = 64: persistent kernel (tatn_fwd1.cuh)
+#endif
+template <bool BF16, bool OUT_F32, bool DROP>
+cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
+                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
+  using Cfg = tatn_dev::Fwd1Cfg;
+  auto kern = tatn_dev::tatn_fwd1_kernel<BF16, OUT_F32, DROP>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -159,11 +182,38 @@ cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
     attr_set = true;
   }
   tatn_dev::FwdParams pp = p;
-  pp.n_pairs = (p.Nq + 128 * NQ - 1) / (128 * NQ);  // Q-tile groups (of NQ tiles) per head
-  pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * D * 4.0, NQ == 2 ? 1 : 2);
-  dim3 grid(static_cast<unsigned>(p.B * p.H * pp.n_pairs));
-  kern<<<grid, tatn_dev::fwd_threads<NQ>(), Cfg::kSmemBytes, stream>>>(q, k, v, o, pp);
+  pp.n_pairs = (p.Nq + 127) / 128;  // Q tiles per (b, h)
+  pp.n_items = p.B * p.H * pp.n_pairs;
+  pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * 64 * 4.0, 2);
+  int* ctr = fwd_counter();
+  if (ctr == nullptr) return cudaErrorInvalidValue;
+  // dense: persistent, two CTAs per SM; block-sparse: one CTA per item
+  const int grid = p.grid != nullptr ? pp.n_items : std::min(pp.n_items, 2 * tatn_host::sm_count());
+  kern<<<grid, 192, Cfg::kSmemBytes, stream>>>(q, k, v, o, pp, ctr);
   return cudaGetLastError();
+}
+
+template <int D, bool BF16, bool OUT_F32, bool DROP, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
+cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
+                       const tatn_dev::FwdParams& p, cudaStream_t stream) {
+  if constexpr (D == 64 && TATN_FWD_PERSISTENT) {
+    return launch_fwd1<BF16, OUT_F32, DROP>(q, k, v, o, p, stream);
+  } else {
+    using Cfg = tatn_dev::FwdCfg<D, NQ>;
+    auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ, DROP>;
+    static bool attr_set = false;  // benign race: idempotent
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    tatn_dev::FwdParams pp = p;
+    pp.n_pairs = (p.Nq + 128 * NQ - 1) / (128 * NQ);  // Q-tile groups (of NQ tiles) per head
+    pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * D * 4.0, NQ == 2 ? 1 : 2);
+    dim3 grid(static_cast<unsigned>(p.B * p.H * pp.n_pairs));
+    kern<<<grid, tatn_dev::fwd_threads<NQ>(), Cfg::kSmemBytes, stream>>>(q, k, v, o, pp);
+    return cudaGetLastError();
+  }
 }
 
 }  // namespace

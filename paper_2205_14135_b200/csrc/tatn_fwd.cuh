@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
   const int pair = (p.mask_kind == kMaskCausal && p.grid == nullptr) ? (p.n_pairs - 1 - slot) : slot;
   uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
   if (threadIdx.x == 0) TATN_TRACE_AT(0);
+  TATN_EV_INIT();
 
   if (threadIdx.x == 0) {
     mbar_init(BAR(kBarQ), 1);
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
       int t = sc.next(0);
       int stage = 0;
       uint32_t ph = 0, fph = 0, pph1 = 0;
+      int mt = 0;  // tiles issued (trace index)
       if (t < sc.T) {
         mbar_wait(BAR(kBarKFull + 0), 0);
         tc_fence_after();
@@ -319,11 +321,14 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
           issue_qk(0, tn, sn);
           if (elect_one_sync()) mma_commit(BAR(kBarKEmpty + sn));
           __syncwarp();
+          if (lane == 0) TATN_EV(mt + 1, 4);
         }
         mbar_wait(BAR(kBarPFull + 0), pph1);
         pph1 ^= 1;
+        if (lane == 0) TATN_EV(mt, 3);
         mbar_wait(BAR(kBarVFull + stage), ph);
         tc_fence_after();
+        if (lane == 0) TATN_EV(mt, 5);
         if (elect_one_sync()) {
 #pragma unroll
           for (int kk = 0; kk < kBN / 16; ++kk)
@@ -337,6 +342,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         t = tn;
         stage = sn;
         ph = phn;
+        ++mt;
       }
       if (elect_one_sync()) mma_commit(BAR(kBarOFinal + 0));
       __syncwarp();
@@ -489,6 +495,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         mbar_wait(BAR(kBarSFull + 0), sph);
         sph ^= 1;
         tc_fence_after();
+        if (threadIdx.x == 0) TATN_EV(n_done, 0);
         if (threadIdx.x == 0 && n_done == 0) TATN_TRACE_AT(1);
         if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(8);
         if (threadIdx.x == 0 && n_done == 3) TATN_TRACE_AT(13);
@@ -503,6 +510,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         tmem_ld_wait32(sv[3]);
         tc_fence_before();
         mbar_arrive(BAR(kBarSFree));
+        if (threadIdx.x == 0) TATN_EV(n_done, 1);
         const int k0 = t * kBN;
         const bool need_mask = (k0 + kBN > sc.kv_limit) || (causal && k0 + kBN - 1 > my_q0c) || custom_on;
         const int lim = min(sc.kv_limit, causal ? growc + 1 : sc.kv_limit) - k0;  // columns >= lim are masked
@@ -599,6 +607,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(BAR(kBarPFull + 0));
+        if (threadIdx.x == 0) TATN_EV(n_done, 2);
         if (threadIdx.x == 0) TATN_TRACE_AT(2);
         if (threadIdx.x == 0 && n_done == 2) TATN_TRACE_AT(10);
         ++n_done;

@@ -18,6 +18,7 @@ struct FwdParams {
   uint32_t* visited;         // optional tr*tc bitmap of tiles the kernel computed
   float* lse;                // [B, H, Nq] natural-log logsumexp (fp32)
   int n_pairs;               // ceil(Nq / 256): CTAs per (b, h)
+  int n_items;               // persistent d = 64 kernel: B * H * ceil(Nq / 128) work items
   int group;                 // heads per scheduling group (CTA order, see tatn_fwd_kernel)
   uint64_t drop_seed;        // dropout: slice (b, h) uses mix64 chains from drop_seed + b*H + h
   uint64_t drop_thresh;      // keep iff hash >= drop_thresh  (= ceil(p * 2^53) << 11)
