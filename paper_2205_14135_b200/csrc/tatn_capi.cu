@@ -187,8 +187,8 @@ cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * 64 * 4.0, 2);
   int* ctr = fwd_counter();
   if (ctr == nullptr) return cudaErrorInvalidValue;
-  // dense: persistent, two CTAs per SM; block-sparse: one CTA per item
-  const int grid = p.grid != nullptr ? pp.n_items : std::min(pp.n_items, 2 * tatn_host::sm_count());
+  // persistent: two CTAs per SM
+  const int grid = std::min(pp.n_items, 2 * tatn_host::sm_count());
   kern<<<grid, 192, Cfg::kSmemBytes, stream>>>(q, k, v, o, pp, ctr);
   return cudaGetLastError();
 }

@@ -11,9 +11,9 @@
 //     first) is issued as soon as the softmax has pulled S into registers;
 //   * the softmax warpgroup writes item n's O (staged in item n's Q buffer, TMA store) and goes
 //     straight on to item n+1's first tile, whose S is already computed.
-// Dense launches claim items from a self-resetting device counter (the last CTA to finish zeroes
-// it for the next launch); block-sparse launches keep one item per CTA (item = blockIdx.x), whose
-// grid row is read once into a shared-memory bitmask.
+// Items are claimed from a self-resetting device counter (the last CTA to finish zeroes it for the
+// next launch). Block-sparse launches: the producer reads the claimed item's grid row into a
+// shared-memory bitmask slot (one per ring slot) before publishing the item.
 #pragma once
 
 #include "tatn_fwd.cuh"
@@ -29,8 +29,8 @@ struct Fwd1Cfg {
   static constexpr int kOffV = kOffK + kStages * kTileBytes;
   static constexpr int kOffBar = kOffV + kStages * kTileBytes;
   static constexpr int kOffRing = kOffBar + 256;
-  static constexpr int kOffMask = kOffRing + 64;  // block-sparse grid row bitmask (64 words)
-  static constexpr int kSmemBytes = kOffMask + 256 + 1024;
+  static constexpr int kOffMask = kOffRing + 64;  // block-sparse grid row bitmasks, 64 words per ring slot
+  static constexpr int kSmemBytes = kOffMask + 4 * 256 + 1024;
   static constexpr uint32_t kTmemS = 0, kTmemO = 128, kTmemP = 192, kTmemCols = 256;
   static constexpr int kRing = 4;
 };
@@ -88,16 +88,6 @@ __global__ void __launch_bounds__(192, 2)
     tmem_alloc(smem_u32(tmem_slot), Cfg::kTmemCols);
     tmem_relinquish();
   }
-  if (sparse && warp == kProducerWarp) {  // one item per CTA: its grid row as a bitmask
-    int bh0, qt0;
-    fwd1_item(p, static_cast<int>(blockIdx.x), bh0, qt0);
-    const uint8_t* row = qt0 < p.tr ? p.grid + static_cast<size_t>(qt0) * p.tc : nullptr;
-    for (int base = 0; base < p.tc; base += 32) {
-      const int t = base + lane;
-      const uint32_t bits = __ballot_sync(0xffffffffu, row != nullptr && t < p.tc && row[t] != 0);
-      if (lane == 0) mask_smem[base >> 5] = bits;
-    }
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -106,9 +96,11 @@ __global__ void __launch_bounds__(192, 2)
   // per-item schedule (identical in every role)
   struct Item {
     int bh, b, h, q0, T, kv_limit;
+    const uint32_t* mask;  // block-sparse: the item's grid row bitmask (ring slot)
   };
-  auto item = [&](int w) {
+  auto item = [&](int w, int n) {
     Item it;
+    it.mask = mask_smem + (n % Cfg::kRing) * 64;
     int qt;
     fwd1_item(p, w, it.bh, qt);
     it.b = it.bh / p.H;
@@ -118,19 +110,19 @@ __global__ void __launch_bounds__(192, 2)
     if (p.mask_kind == kMaskKeyPadding && p.valid_len != nullptr)
       kv_limit = min(kv_limit, max(p.valid_len[it.b] - p.k_off, 0));
     it.kv_limit = kv_limit;
-    int n = (kv_limit + kBN - 1) / kBN;
+    int nt = (kv_limit + kBN - 1) / kBN;
     if (p.mask_kind == kMaskCausal) {
       const int last = it.q0 + kBM - 1 - p.k_off;
-      n = min(n, last >= 0 ? last / kBN + 1 : 0);
+      nt = min(nt, last >= 0 ? last / kBN + 1 : 0);
     }
-    it.T = sparse ? p.tc : (it.q0 < p.Nq ? n : 0);
+    it.T = sparse ? p.tc : (it.q0 < p.Nq ? nt : 0);
     return it;
   };
   // first visited key tile >= t of an item (T when none)
   auto next_tile = [&](const Item& it, int t) -> int {
     if (!sparse) return t;
     while (t < it.T) {
-      const uint32_t m = mask_smem[t >> 5] >> (t & 31);
+      const uint32_t m = it.mask[t >> 5] >> (t & 31);
       if (m) return t + __ffs(m) - 1;
       t = ((t >> 5) + 1) << 5;
     }
@@ -158,17 +150,28 @@ __global__ void __launch_bounds__(192, 2)
       if (n >= Cfg::kRing)
         mbar_wait(BAR(kBarItemFree + n % Cfg::kRing), static_cast<uint32_t>((n / Cfg::kRing - 1) & 1));
       int w = -1;
-      if (sparse) w = (n == 0) ? static_cast<int>(blockIdx.x) : -1;
-      else if (lane == 0) w = atomicAdd(ctr, 1);
+      if (lane == 0) w = atomicAdd(ctr, 1);
       w = __shfl_sync(0xffffffffu, w, 0);
       if (w >= p.n_items) w = -1;
+      if (sparse && w >= 0) {  // the item's grid row -> bitmask slot n % kRing (read once, coalesced)
+        int bh0, qt0;
+        fwd1_item(p, w, bh0, qt0);
+        const uint8_t* grow_ptr = qt0 < p.tr ? p.grid + static_cast<size_t>(qt0) * p.tc : nullptr;
+        uint32_t* slot_mask = mask_smem + (n % Cfg::kRing) * 64;
+        for (int base = 0; base < p.tc; base += 32) {
+          const int t = base + lane;
+          const uint32_t bits = __ballot_sync(0xffffffffu, grow_ptr != nullptr && t < p.tc && grow_ptr[t] != 0);
+          if (lane == 0) slot_mask[base >> 5] = bits;
+        }
+        __syncwarp();
+      }
       if (lane == 0) {
         ring[n % Cfg::kRing] = w;
         mbar_arrive(BAR(kBarItem + n % Cfg::kRing));
       }
       __syncwarp();
       if (w < 0) break;
-      const Item it = item(w);
+      const Item it = item(w, n);
       const int qb = n & 1;
       if (n >= 2) mbar_wait(BAR(kBarQFree + qb), static_cast<uint32_t>(((n >> 1) - 1) & 1));
       if (elect_one_sync()) {
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(192, 2)
         if (w < 0) return false;
         ps.n = n_taken++;
         ps.w = w;
-        ps.it = item(w);
+        ps.it = item(w, ps.n);
         ps.t = next_tile(ps.it, 0);
         ps.first = 1;
         if (ps.t < ps.it.T) return true;
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(192, 2)
     for (int n = 0;; ++n) {
       const int w = take_item(n);
       if (w < 0) break;
-      const Item it = item(w);
+      const Item it = item(w, n);
       const int qb = n & 1;
       const int grow = it.q0 + row;
       const int growc = grow - p.k_off;
@@ -496,7 +499,7 @@ __global__ void __launch_bounds__(192, 2)
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0 && !sparse) {
+  if (threadIdx.x == 0) {
     // self-resetting counter: the last CTA to finish (every claim done) zeroes it for the next launch
     __threadfence();
     if (atomicAdd(ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {

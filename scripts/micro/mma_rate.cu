@@ -58,10 +58,79 @@ void run(int R) {
          e == cudaSuccess ? "" : cudaGetErrorString(e));
   cudaFree(d);
 }
+
+// The backward's per-Q-tile MMA stream at d = 64 (dV, dK TS N=64; S^T, dP^T SS N=64; dQ^T SS M=64),
+// R times back to back: cycles per tile-equivalent (24 MMAs; ideal 1024 at 128 B/clk smem).
+__global__ void __launch_bounds__(128, 1) kmix(unsigned long long* out, int R, int variant) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t base = smem_u32(sm);
+  for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) st_shared_v4(base + 16 * i, 0, 0, 0, 0);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); fence_mbar_init(); }
+  if (threadIdx.x < 32) { tmem_alloc(smem_u32(&slot), 512); tmem_relinquish(); }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  if (threadIdx.x < 32) {
+    const uint64_t dA = make_sdesc_sw128(base, 16, 1024);            // K-major A (K or V)
+    const uint64_t dB = make_sdesc_sw128(base + 32768, 16, 1024);    // K-major B (Q or dO)
+    const uint64_t dBmn = make_sdesc_sw128(base + 32768, 8192, 1024);
+    const uint64_t dAmn = make_sdesc_sw128(base, 16384, 1024);
+    constexpr uint32_t id_s = make_idesc_f16(1, 128, 64, 0, 0);
+    constexpr uint32_t id_acc = make_idesc_f16(1, 128, 64, 0, 1);
+    constexpr uint32_t id_dq = make_idesc_f16(1, 64, 64, 1, 1);
+    unsigned long long t0 = clock64();
+    if (elect_one_sync()) {
+      for (int r = 0; r < R; ++r) {
+        const uint32_t x = (r & 1) * 128;
+        if (variant == 0 || variant == 1) {
+          for (int kk = 0; kk < 4; ++kk) mma_ts(tm + 256, tm + x + kk * 8, dBmn + ((kk * 2048) >> 4), id_acc, 1u);  // dV
+          for (int kk = 0; kk < 4; ++kk) mma_ts(tm + 320, tm + x + 64 + kk * 8, dBmn + ((kk * 2048) >> 4), id_acc, 1u);  // dK
+        }
+        if (variant == 0 || variant == 2) {
+          for (int kk = 0; kk < 4; ++kk) mma_ss(tm + x + 64, dA + ((kk * 32) >> 4), dB + ((kk * 32) >> 4), id_s, kk > 0);  // dP^T
+          for (int kk = 0; kk < 4; ++kk) mma_ss(tm + x, dA + ((kk * 32) >> 4), dB + ((kk * 32) >> 4), id_s, kk > 0);  // S^T
+        }
+        if (variant == 0 || variant == 3)
+          for (int kk = 0; kk < 8; ++kk) mma_ss(tm + 384 + (r & 1) * 64, dAmn + ((kk * 2048) >> 4), dBmn + ((kk * 2048) >> 4), id_dq, kk > 0);  // dQ^T
+      }
+      mma_commit(smem_u32(&bar));
+    }
+    __syncwarp();
+    mbar_wait(smem_u32(&bar), 0);
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tm, 512); }
+}
+void runmix(int R) {
+  unsigned long long* d; cudaMalloc(&d, 148 * 8);
+  cudaFuncSetAttribute(kmix, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
+  const char* names[4] = {"full tile (24 MMAs)", "dV+dK TS (8)", "S^T+dP^T SS (8)", "dQ^T M=64 SS (8)"};
+  const int cnt[4] = {24, 8, 8, 8};
+  for (int v = 0; v < 4; ++v) {
+    kmix<<<148, 128, 65536 + 1024>>>(d, 16, v);
+    cudaDeviceSynchronize();
+    kmix<<<148, 128, 65536 + 1024>>>(d, R, v);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    double s = 0; for (int i = 0; i < 148; ++i) s += h[i];
+    printf("bwd stream %-22s: %7.1f cycles per tile, %5.1f per MMA %s\n", names[v], s / 148 / R, s / 148 / R / cnt[v],
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+  }
+  cudaFree(d);
+}
+
 int main() {
   const int R = 4096;
   run<32, false>(R); run<64, false>(R); run<128, false>(R); run<256, false>(R);
   run<32, true>(R); run<64, true>(R); run<128, true>(R); run<256, true>(R);
+  runmix(512);
   run<64, false, 64, 0>(R); run<64, false, 64, 1>(R); run<64, false, 128, 1>(R); run<128, false, 64, 1>(R);
   return 0;
 }
