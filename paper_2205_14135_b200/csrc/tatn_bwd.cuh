@@ -70,8 +70,11 @@ struct BwdCfg {
   static constexpr int kOffVec = kOffDQ + kDQBytes;
   static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
   static constexpr int kOffRing = kOffBar + 384;       // item ring (kItemRing ints)
-  static constexpr int kOffMask = kOffRing + 64;       // block-sparse q-tile bitmask, 128 words
-  static constexpr int kOffDrop = kOffMask + 512;      // dropout: 64 query-row hashes per softmax warpgroup
+  static constexpr int kOffMask = kOffRing + 64;       // block-sparse q-tile bitmasks, 128 words each
+  // d = 64: one bitmask per item-ring slot (block-sparse launches run persistent too);
+  // d = 128 has no shared memory left for them: block-sparse runs one item per CTA
+  static constexpr int kMaskSlots = (D == 64) ? 4 : 1;
+  static constexpr int kOffDrop = kOffMask + 512 * kMaskSlots;  // dropout: 64 query-row hashes per softmax warpgroup
   static constexpr int kSmemBytes = kOffDrop + (DROP ? 1024 : 0);  // dynamic smem is declared __align__(1024)
   static_assert(kSmemBytes <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
   static_assert(2 * 128 * D * 2 <= kOffVec - kOffDS, "dK/dV staging must fit the dS^T + dQ staging region");
@@ -364,22 +367,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_relinquish();
   }
-  // block-sparse launches run one item per CTA (grid = items): its grid column is read once
-  // into a bitmask over 64-row Q tiles
-  if (p.grid != nullptr && warp == kProducerWarp) {
+  // block-sparse grid column of item w (key tile j) -> bitmask over 64-row Q tiles, read once
+  auto build_col_mask = [&](int w, uint32_t* dst) {  // whole producer warp
     int bh0, j0;
-    bwd_item(p, static_cast<int>(blockIdx.x), bh0, j0);
+    bwd_item(p, w, bh0, j0);
     const uint8_t* gcol = p.grid + j0;
     for (int base = 0; base < p.tr; base += 32) {
       const int r = base + lane;
       const bool v = r < p.tr && gcol[static_cast<size_t>(r) * p.tc] != 0;
       const uint32_t bits = __ballot_sync(0xffffffffu, v);
       if (lane == 0) {
-        mask_smem[(2 * base) >> 5] = spread_bits16(bits);
-        mask_smem[((2 * base) >> 5) + 1] = spread_bits16(bits >> 16);
+        dst[(2 * base) >> 5] = spread_bits16(bits);
+        dst[((2 * base) >> 5) + 1] = spread_bits16(bits >> 16);
       }
     }
-  }
+    __syncwarp();
+  };
+  constexpr bool kSparsePersistent = Cfg::kMaskSlots == kItemRing;
+  // d = 128 block-sparse launches run one item per CTA (grid = items)
+  if (!kSparsePersistent && p.grid != nullptr && warp == kProducerWarp) build_col_mask(static_cast<int>(blockIdx.x), mask_smem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -390,13 +396,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int bh, b, h, j, cnt;
     BwdSched sc;
   };
-  auto item = [&](int w) {
+  auto item = [&](int w, int n) {
     Item it;
     bwd_item(p, w, it.bh, it.j);
     it.b = it.bh / p.H;
     it.h = it.bh - it.b * p.H;
     it.sc = make_bwd_sched(p, it.b, it.j);
-    it.sc.mask = mask_smem;
+    it.sc.mask = mask_smem + (kSparsePersistent ? (n % kItemRing) * 128 : 0);
     it.cnt = 0;
     if (it.sc.gcol == nullptr) it.cnt = it.sc.i_end - it.sc.i_begin;
     else
@@ -420,20 +426,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (n >= kItemRing)
         mbar_wait(BAR(kBarItemFree + n % kItemRing), static_cast<uint32_t>((n / kItemRing - 1) & 1));
       int w = -1;
-      if (p.grid != nullptr) {
+      if (p.grid != nullptr && !kSparsePersistent) {
         w = (n == 0) ? static_cast<int>(blockIdx.x) : -1;
       } else if (lane == 0) {
         w = atomicAdd(p.item_counter, 1);
       }
       w = __shfl_sync(0xffffffffu, w, 0);
       if (w >= p.n_items) w = -1;
+      if (kSparsePersistent && p.grid != nullptr && w >= 0) build_col_mask(w, mask_smem + (n % kItemRing) * 128);
       if (lane == 0) {
         ring[n % kItemRing] = w;
         mbar_arrive(BAR(kBarItem + n % kItemRing));
       }
       __syncwarp();
       if (w < 0) break;
-      const Item it = item(w);
+      const Item it = item(w, n);
       const int kb = n % NKV;
       if (n >= NKV) mbar_wait(BAR(kBarKVFree + kb), static_cast<uint32_t>((n / NKV - 1) & 1));
       if (elect_one_sync()) {
@@ -490,7 +497,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int n = 0;; ++n) {
       const int w = take_item(n);
       if (w < 0) break;
-      const int cnt = item(w).cnt;
+      const int cnt = item(w, n).cnt;
       const int kb = n % NKV;
       const uint32_t koff = static_cast<uint32_t>(kb * 2 * Cfg::kKVTile);  // K of buffer kb
       const uint32_t voff = koff + Cfg::kKVTile;
@@ -637,7 +644,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int n = 0;; ++n) {
       const int w = take_item(n);
       if (w < 0) break;
-      const Item it = item(w);
+      const Item it = item(w, n);
       const BwdSched& sc = it.sc;
       const int kj = sc.k0 + r;
       bool first = true;  // first dS^T store of this warpgroup in this item
@@ -788,7 +795,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int n = 0;; ++n) {
       const int w = take_item(n);
       if (w < 0) break;
-      const Item it = item(w);
+      const Item it = item(w, n);
       for (int i = it.sc.next(it.sc.i_begin); i < it.sc.i_end; i = it.sc.next(i + 1), ++g) {
         const int x = g & 1;
         mbar_wait(BAR(kBarDQFull + x), static_cast<uint32_t>((g >> 1) & 1));
@@ -1022,10 +1029,12 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  // dense: persistent, one CTA per SM looping over items; block-sparse: one CTA per item
-  // (the grid column is read once into a shared-memory bitmask)
+  // persistent, one CTA per SM looping over items (d = 128 block-sparse: one CTA per item, the grid
+  // column read once into a shared-memory bitmask)
   const int n_sm = tatn_host::sm_count();
-  dim3 grid(static_cast<unsigned>(d.block_grid != nullptr ? p.n_items : std::min(p.n_items, n_sm)));
+  dim3 grid(static_cast<unsigned>((d.block_grid != nullptr && !(Cfg::kMaskSlots == tatn_dev::kItemRing))
+                                       ? p.n_items
+                                       : std::min(p.n_items, n_sm)));
   cudaEvent_t prof_stop = tatn_host::profile_begin(1, stream);
   kern<<<grid, tatn_dev::kBwdThreads, Cfg::kSmemBytes, stream>>>(mq, mk, mv, mdo, mdk, mdv, p, lse2, Nq_pad);
   if (prof_stop) cudaEventRecord(prof_stop, stream);
