@@ -84,6 +84,16 @@ struct FwdSched {
     if (sparse) return (mask[q][t >> 5] >> (t & 31)) & 1u;
     return t < nkv[q];
   }
+  // does Q tile q visit any tile after t?
+  __device__ __forceinline__ bool has_after(int q, int t) const {
+    if (!sparse) return t + 1 < nkv[q];
+    for (int u = t + 1; u < T;) {
+      const uint32_t m = mask[q][u >> 5] >> (u & 31);
+      if (m) return true;
+      u = ((u >> 5) + 1) << 5;
+    }
+    return false;
+  }
   // first tile >= t visited by either Q tile (T when none)
   __device__ __forceinline__ int next(int t) const {
     if (!sparse) return t;
@@ -355,6 +365,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
     int t = sc.next(0);
     int stage = 0;
     uint32_t ph = 0;
+    bool ofinal_done[2] = {false, false};
 #ifdef TATN_TRACE
     int dbg_pv = 0;
 #endif
@@ -395,6 +406,11 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         }
         __syncwarp();
         acc[q] = 1;
+        if (!sc.has_after(q, t)) {  // last PV of tile q: its epilogue may start under the other tile's work
+          if (elect_one_sync()) mma_commit(BAR(kBarOFinal + q));
+          __syncwarp();
+          ofinal_done[q] = true;
+        }
         if (tn < sc.T && sc.member(q, tn)) {
           if (!k_ready) {
             mbar_wait(BAR(kBarKFull + sn), phn);
@@ -429,7 +445,8 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
       ph = phn;
     }
     if (elect_one_sync())
-      for (int q = 0; q < NQ; ++q) mma_commit(BAR(kBarOFinal + q));
+      for (int q = 0; q < NQ; ++q)
+        if (!ofinal_done[q]) mma_commit(BAR(kBarOFinal + q));
     __syncwarp();
     }  // NQ == 2
   }
