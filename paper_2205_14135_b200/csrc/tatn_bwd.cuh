@@ -1012,7 +1012,10 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.custom_t_words = custom_t_words;
   p.custom_t_b = (custom && d.custom_bstride != 0) ? 1 : 0;
   p.k_off = d.k_offset;
-  p.group = tatn_host::schedule_group(d.B * d.H, p.n_ktiles, static_cast<double>(d.Nq) * D * 8.0, 1);
+  // persistent + dynamic claims: one head group (global longest-first order) unless the heads'
+  // Q / dO / dQ accumulators would not stay L2-resident (block-sparse d = 128: one CTA per item)
+  p.group = tatn_host::schedule_group(d.B * d.H, (d.block_grid != nullptr && D == 128) ? p.n_ktiles : 1,
+                                      static_cast<double>(d.Nq) * D * 8.0, 1);
   p.dk_f32 = OUT_F32 ? static_cast<float*>(dk) : nullptr;
   p.dv_f32 = OUT_F32 ? static_cast<float*>(dv) : nullptr;
   p.k_sb = d.k_str[0];

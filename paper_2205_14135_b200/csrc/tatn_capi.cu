@@ -184,7 +184,9 @@ cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   tatn_dev::FwdParams pp = p;
   pp.n_pairs = (p.Nq + 127) / 128;  // Q tiles per (b, h)
   pp.n_items = p.B * p.H * pp.n_pairs;
-  pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * 64 * 4.0, 2);
+  // persistent + dynamic claims: one head group (global longest-first order) unless the heads'
+  // K/V would not stay L2-resident, so no group boundary brings heavy items back into the tail
+  pp.group = schedule_group(p.B * p.H, 1, static_cast<double>(p.Nk) * 64 * 4.0, 2);
   int* ctr = fwd_counter();
   if (ctr == nullptr) return cudaErrorInvalidValue;
   // persistent: two CTAs per SM

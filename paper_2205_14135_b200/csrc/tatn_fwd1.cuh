@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(192, 2)
   const int lane = static_cast<int>(lane_id());
   const bool sparse = p.grid != nullptr;
   TATN_EV_INIT();
+  if (threadIdx.x == 0) TATN_TRACE_AT(0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
@@ -500,6 +501,12 @@ __global__ void __launch_bounds__(192, 2)
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) {
+    TATN_TRACE_AT(7);
+#ifdef TATN_TRACE
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    if (g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 5] = smid;
+#endif
     // self-resetting counter: the last CTA to finish (every claim done) zeroes it for the next launch
     __threadfence();
     if (atomicAdd(ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
