@@ -46,6 +46,10 @@
 namespace tatn_dev {
 
 constexpr int kBwdThreads = 448;
+#ifndef TATN_BWD_EMU_PAIRS
+#define TATN_BWD_EMU_PAIRS 0  // exp2 pairs per 8 computed by the FMA-pipe polynomial (unmasked tiles)
+#endif
+constexpr int kBwdEmuPairs = TATN_BWD_EMU_PAIRS;
 constexpr int kBwdQT = 64;    // query rows per Q tile
 constexpr int kBwdKT = 128;   // keys per CTA
 
@@ -714,9 +718,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 const uint64_t xv = f2_fma(f2_pack(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sl2x2,
                                            e ? l4.y : l4.x);
                 float p0, p1;
-                f2_unpack(xv, p0, p1);
-                p0 = ex2_approx(p0);
-                p1 = ex2_approx(p1);
+                if (!kMasked && !DROP && kBwdEmuPairs > 0 && (k & 7) < kBwdEmuPairs) {
+                  f2_unpack(exp2_poly_f2(xv), p0, p1);  // FMA pipe: relieves MUFU (x <= 0 here)
+                } else {
+                  f2_unpack(xv, p0, p1);
+                  p0 = ex2_approx(p0);
+                  p1 = ex2_approx(p1);
+                }
                 if constexpr (kMasked) {
                   const uint32_t cwv = (c < 32) ? cbits.x : cbits.y;
                   p0 = (c < c_lo || ((cwv >> (c & 31)) & 1u) == 0u) ? 0.f : p0;

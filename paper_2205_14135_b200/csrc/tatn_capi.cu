@@ -21,6 +21,7 @@
 #include "tatn_bwd.cuh"
 #include "tatn_fwd.cuh"
 #include "tatn_fwd1.cuh"
+#include "tatn_fwd2.cuh"
 
 namespace tatn_host {
 int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm = 1);
@@ -170,6 +171,9 @@ CUtensorMapDataType tma_dtype(int dtype) {
 #ifndef TATN_FWD_PERSISTENT
 #define TATN_FWD_PERSISTENT 1  // d = 64: persistent kernel (tatn_fwd1.cuh)
 #endif
+#ifndef TATN_FWD2_PERSISTENT
+#define TATN_FWD2_PERSISTENT 1  // d = 128: persistent kernel (tatn_fwd2.cuh)
+#endif
 template <bool BF16, bool OUT_F32, bool DROP>
 cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                         const tatn_dev::FwdParams& p, cudaStream_t stream) {
@@ -195,11 +199,35 @@ cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   return cudaGetLastError();
 }
 
+template <bool BF16, bool OUT_F32, bool DROP>
+cudaError_t launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
+  using Cfg = tatn_dev::Fwd2Cfg<128>;
+  auto kern = tatn_dev::tatn_fwd2_kernel<128, BF16, OUT_F32, DROP>;
+  static bool attr_set = false;  // benign race: idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  tatn_dev::FwdParams pp = p;
+  pp.n_pairs = (p.Nq + 255) / 256;  // Q-tile pairs per (b, h)
+  pp.n_items = p.B * p.H * pp.n_pairs;
+  pp.group = schedule_group(p.B * p.H, 1, static_cast<double>(p.Nk) * 128 * 4.0, 1);
+  int* ctr = fwd_counter();
+  if (ctr == nullptr) return cudaErrorInvalidValue;
+  const int grid = std::min(pp.n_items, tatn_host::sm_count());  // persistent, one CTA per SM
+  kern<<<grid, 384, Cfg::kSmemBytes, stream>>>(q, k, v, pp, ctr);
+  return cudaGetLastError();
+}
+
 template <int D, bool BF16, bool OUT_F32, bool DROP, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
 cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
   if constexpr (D == 64 && TATN_FWD_PERSISTENT) {
     return launch_fwd1<BF16, OUT_F32, DROP>(q, k, v, o, p, stream);
+  } else if constexpr (D == 128 && TATN_FWD2_PERSISTENT) {
+    return launch_fwd2<BF16, OUT_F32, DROP>(q, k, v, p, stream);
   } else {
     using Cfg = tatn_dev::FwdCfg<D, NQ>;
     auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ, DROP>;
@@ -357,6 +385,7 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   cudaError_t e;
   const bool f32 = d.out_dtype == TATN_OUT_FP32;
   p.o_f32 = f32 ? static_cast<float*>(o) : nullptr;
+  p.o16 = f32 ? nullptr : o;
   p.o_sb = d.o_str[0];
   p.o_sh = d.o_str[1];
   p.o_sn = d.o_str[2];

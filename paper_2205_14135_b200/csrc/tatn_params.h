@@ -24,6 +24,7 @@ struct FwdParams {
   uint64_t drop_thresh;      // keep iff hash >= drop_thresh  (= ceil(p * 2^53) << 11)
   float drop_scale;          // 1 / (1 - p)
   float* o_f32;              // fp32 output mode: O written here directly (strides below)
+  void* o16;                 // 16-bit O (the persistent d = 128 kernel stores rows directly; strides below)
   int64_t o_sb, o_sh, o_sn;
   const uint32_t* custom;    // Custom mask: keep bits [Nq][custom_words] per batch element (or shared)
   int custom_words;

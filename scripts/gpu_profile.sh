@@ -12,9 +12,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     python bench.py --steps 3 --warmup 3 --no-sweep --no-cpu-baseline --no-graph > /dev/null 2>&1
 mkdir -p /tmp/ncu
 for k in bwd fwd; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tatn_${k}1?_kernel -s 3 -c 1 -o /tmp/ncu/prof_${k}_gpt2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tatn_${k}[12]?_kernel -s 3 -c 1 -o /tmp/ncu/prof_${k}_gpt2 \
       python bench.py --steps 1 --warmup 3 --no-sweep --no-cpu-baseline --no-graph > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tatn_${k}1?_kernel -s 1 -c 1 -o /tmp/ncu/prof_${k}_16k \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tatn_${k}[12]?_kernel -s 1 -c 1 -o /tmp/ncu/prof_${k}_16k \
       python bench.py --workload long-16k --steps 1 --warmup 3 --no-sweep --no-cpu-baseline --no-graph > /dev/null 2>&1
 done
 for r in /tmp/ncu/*.ncu-rep; do
