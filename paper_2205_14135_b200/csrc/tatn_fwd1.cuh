@@ -232,12 +232,18 @@ __global__ void __launch_bounds__(192, 2)
       }
       return next_item(ps);
     };
+    // Every item (also one without tiles) completes one QFull phase of buffer n & 1; they are
+    // waited strictly in item order, so a parity wait is never two phases ahead of its barrier.
+    int q_waited = -1;
+    auto sync_q = [&](int upto) {
+      for (int i = q_waited + 1; i <= upto; ++i)
+        mbar_wait(BAR(kBarQFull + (i & 1)), static_cast<uint32_t>((i >> 1) & 1));
+      if (upto > q_waited) q_waited = upto;
+    };
     auto issue_qk = [&](const Pos& ps, int g) {
       const int stage = g & 1;
       const int qb = ps.n & 1;
-      if (ps.first) {
-        mbar_wait(BAR(kBarQFull + qb), static_cast<uint32_t>((ps.n >> 1) & 1));
-      }
+      if (ps.first) sync_q(ps.n);
       mbar_wait(BAR(kBarKFull + stage), static_cast<uint32_t>((g >> 1) & 1));
       tc_fence_after();
       if (elect_one_sync()) {
@@ -254,6 +260,24 @@ __global__ void __launch_bounds__(192, 2)
       }
       __syncwarp();
     };
+    auto issue_pv = [&](const Pos& ps, int g, bool last_of_item) {
+      mbar_wait(BAR(kBarPFull), static_cast<uint32_t>(g & 1));
+      if (lane == 0) TATN_EV(g, 3);
+      const int stage = g & 1;
+      mbar_wait(BAR(kBarVFull + stage), static_cast<uint32_t>((g >> 1) & 1));
+      tc_fence_after();
+      if (elect_one_sync()) {
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          mma_ts(tmem_base + Cfg::kTmemO, tmem_base + Cfg::kTmemP + kk * 8,
+                 vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv,
+                 (ps.first ? 0u : 1u) | (kk > 0 ? 1u : 0u));
+        mma_commit(BAR(kBarPVDone));
+        mma_commit(BAR(kBarVEmpty + stage));
+        if (last_of_item) mma_commit(BAR(kBarOFinal));
+      }
+      __syncwarp();
+    };
     Pos cur;
     if (next_item(cur)) {
       int g = 0;  // global tile index of `cur`
@@ -261,32 +285,26 @@ __global__ void __launch_bounds__(192, 2)
       for (;;) {
         Pos nx = cur;
         const bool has_next = advance(nx);
-        if (has_next) {
+        // QK of the next tile is issued before PV(cur) (it runs under softmax(cur)) unless it
+        // belongs to an item two or more items ahead: that item's Q reuses cur's Q buffer, which
+        // is reloaded only after cur's epilogue, i.e. after PV(cur).
+        const bool early = has_next && nx.n <= cur.n + 1;
+        if (early) {
           mbar_wait(BAR(kBarSFree), static_cast<uint32_t>(g & 1));  // S(g) is in registers
           issue_qk(nx, g + 1);
           if (lane == 0) TATN_EV(g + 1, 4);
         }
-        mbar_wait(BAR(kBarPFull), static_cast<uint32_t>(g & 1));
-        if (lane == 0) TATN_EV(g, 3);
-        const int stage = g & 1;
-        mbar_wait(BAR(kBarVFull + stage), static_cast<uint32_t>((g >> 1) & 1));
-        tc_fence_after();
-        if (elect_one_sync()) {
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk)
-            mma_ts(tmem_base + Cfg::kTmemO, tmem_base + Cfg::kTmemP + kk * 8,
-                   vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv,
-                   (cur.first ? 0u : 1u) | (kk > 0 ? 1u : 0u));
-          mma_commit(BAR(kBarPVDone));
-          mma_commit(BAR(kBarVEmpty + stage));
-          if (!has_next || nx.n != cur.n) mma_commit(BAR(kBarOFinal));  // last tile of the item
+        issue_pv(cur, g, !has_next || nx.n != cur.n);
+        if (has_next && !early) {
+          mbar_wait(BAR(kBarSFree), static_cast<uint32_t>(g & 1));
+          issue_qk(nx, g + 1);
         }
-        __syncwarp();
         if (!has_next) break;
         cur = nx;
         ++g;
       }
     }
+    sync_q(n_taken - 1);  // trailing items without tiles: consume their QFull phases
   } else {
     // ------------------------------------------------------------ softmax + epilogue warpgroup
     const int row = warp * 32 + lane;  // row within the tile == TMEM lane

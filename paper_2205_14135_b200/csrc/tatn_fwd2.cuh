@@ -278,8 +278,10 @@ __global__ void __launch_bounds__(384, 1)
         __syncwarp();
       };
       int t = sc.next(0);
+      // every item consumes a QFull phase (also items without tiles): wait in order, so no wait is
+      // ever two phases ahead of the barrier
+      mbar_wait(BAR(kBarQFull), static_cast<uint32_t>(n & 1));
       if (t < sc.T) {
-        mbar_wait(BAR(kBarQFull), static_cast<uint32_t>(n & 1));
         mbar_wait(BAR(kBarKFull + g % S), static_cast<uint32_t>((g / S) & 1));
         tc_fence_after();
         for (int q = 0; q < 2; ++q)

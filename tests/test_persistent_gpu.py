@@ -1,0 +1,86 @@
+"""Persistent kernels (K1 d=64 / d=128, K3): dynamic item claims from self-resetting device
+counters must give the same results under every launch pattern — back-to-back launches reusing
+a counter, concurrent launches on different streams, far more items than CTAs, items with no
+tiles, and CUDA-graph replay."""
+import numpy as np
+import pytest
+import torch
+
+from tests import gpu_helpers as G
+from paper_2205_14135_b200 import attention as A
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(B, H, N, d, dtype="bf16", seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    dt = G.TORCH_DT[dtype]
+    return [torch.randn((B, H, N, d), generator=g, device="cuda").to(dt) for _ in range(4)]
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_repeated_and_concurrent_launches_agree(cuda_device, d):
+    q, k, v, do = _inputs(4, 8, 777, d)
+    spec = A.AttnSpec(mask="causal")
+    o0, l0 = A.flash_fwd(q, k, v, spec)
+    g0 = A.flash_bwd(q, k, v, o0, do, l0, spec)
+    torch.cuda.synchronize()
+    for _ in range(5):  # the counters reset themselves between launches
+        o1, l1 = A.flash_fwd(q, k, v, spec)
+        assert torch.equal(o1, o0) and torch.equal(l1, l0)
+    # concurrent launches on two streams (distinct counter slots) over different problems
+    q2, k2, v2, do2 = _inputs(2, 16, 1500, d, seed=3)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = {}
+    with torch.cuda.stream(s1):
+        outs["a"] = A.flash_fwd(q, k, v, spec)
+    with torch.cuda.stream(s2):
+        outs["b"] = A.flash_fwd(q2, k2, v2, A.AttnSpec(mask="none"))
+    torch.cuda.synchronize()
+    assert torch.equal(outs["a"][0], o0)
+    ref_b = A.flash_fwd(q2, k2, v2, A.AttnSpec(mask="none"))
+    torch.cuda.synchronize()
+    assert torch.equal(outs["b"][0], ref_b[0])
+    # backward: dK, dV are deterministic; dQ is an fp32 reduction (order may vary)
+    g1 = A.flash_bwd(q, k, v, o0, do, l0, spec)
+    torch.cuda.synchronize()
+    assert torch.equal(g1[1], g0[1]) and torch.equal(g1[2], g0[2])
+    assert torch.allclose(g1[0].float(), g0[0].float(), atol=2e-2, rtol=0)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_many_tiny_items_and_empty_items(cuda_device, d):
+    # 3000 (b, h) slices of one tile each, key padding with some batches fully padded (no tiles)
+    B, H, N = 30, 100, 96
+    q, k, v, do = (G.make_inputs(B, H, N, N, d, "fp16"))
+    vl = np.array([0 if b % 7 == 0 else N - (b % 5) for b in range(B)], dtype=np.int32)
+    got = G.run_gpu(q, k, v, do, "fp16", mask="key_padding", valid_len=vl)
+    ref = G.oracle_full(q, k, v, do, mask="key_padding", valid_len=vl)
+    for key in ("o", "lse", "dq", "dk", "dv"):
+        G.assert_close(key, got[key], ref[key])
+    empty = vl == 0
+    assert np.all(got["o"][empty] == 0) and np.all(np.isneginf(got["lse"][empty]))
+    assert np.all(got["dk"][empty] == 0) and np.all(got["dq"][empty] == 0)
+
+
+def test_graph_replay_matches_eager(cuda_device):
+    q, k, v, do = _inputs(8, 12, 1024, 64)
+    spec = A.AttnSpec(mask="causal")
+    o = torch.empty_like(q)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ws = A.bwd_workspace(q, k, v, spec)
+    step = lambda: (A.flash_fwd(q, k, v, spec, out=o, lse=lse),
+                    A.flash_bwd(q, k, v, o, do, lse, spec, dq, dk, dv, ws))
+    step()
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (o, lse, dk, dv, dq)]
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        step()
+    for _ in range(3):
+        gr.replay()
+    torch.cuda.synchronize()
+    for a, b in zip((o, lse, dk, dv), ref[:4]):
+        assert torch.equal(a, b)
+    assert torch.allclose(dq.float(), ref[4].float(), atol=2e-2, rtol=0)
