@@ -333,7 +333,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int kBarKVFree = kBarKVFull + NKV;  // [NKV] MMAs of the buffer's item done
   const int kBarFinal = kBarKVFree + NKV;   // item's MMAs done (dK, dV final in TMEM)
   const int kBarAccFree = kBarFinal + 1;    // dK / dV drained from TMEM (count 128)
-  const int kBarStageFree = kBarAccFree + 1;// output staging read by the TMA store
+  // slot kBarStageFree is not an mbarrier but a counter: items whose output staging the TMA
+  // store has read (a softmax warpgroup may skip items, so it waits on a count, not a parity)
+  const int kBarStageFree = kBarAccFree + 1;
   const int kBarItem = kBarStageFree + 1;   // [kItemRing] item id published
   const int kBarItemFree = kBarItem + kItemRing;  // [kItemRing] slot read by all 13 consumer warps
   const int kNumBars = kBarItemFree + kItemRing;
@@ -358,7 +360,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   TATN_EV_INIT();
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
+    // (the counter slot is never an mbarrier: an mbarrier init is a SYNCS-unit write that is
+    // not ordered with a plain store to the same word)
+    for (int i = 0; i < kNumBars; ++i)
+      if (i != kBarStageFree) mbar_init(BAR(i), 1);
+    *reinterpret_cast<volatile uint64_t*>(smem_gen + Cfg::kOffBar + 8 * kBarStageFree) = 0;
     for (int x = 0; x < 2; ++x) {
       mbar_init(BAR(kBarPFull + x), Cfg::kSplit ? 256 : 128);
       mbar_init(BAR(kBarDQEmpty + x), 128);
@@ -759,7 +765,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               // the dQ^T MMA of tile g - 2 must have released the dS^T buffer, and in a new
               // item the previous item's dK / dV staging must have been stored
               mbar_wait(BAR(kBarDSEmpty + x), static_cast<uint32_t>(((g >> 1) & 1) ^ 1));
-              if (first && n > 0) mbar_wait(BAR(kBarStageFree), static_cast<uint32_t>((n - 1) & 1));
+              if (first) wait_counter_ge(BAR(kBarStageFree), static_cast<uint32_t>(n));
               first = false;
             }
             // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
@@ -915,7 +921,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           bulk_wait_read_all();
         }
       }
-      if (leader) mbar_arrive(BAR(kBarStageFree));
+      if (leader) st_release_u32(BAR(kBarStageFree), static_cast<uint32_t>(n + 1));
     }
     if (leader) bulk_wait_all();
     if (leader) TATN_TRACE_AT(8);
