@@ -18,6 +18,10 @@
 
 #include "tatn_fwd.cuh"
 
+#ifndef TATN_FWD1_CHUNK_SKIP
+#define TATN_FWD1_CHUNK_SKIP 0  // 1: skip all-masked 32-column chunks of masked tiles (spills at 168 regs: slower)
+#endif
+
 namespace tatn_dev {
 
 struct Fwd1Cfg {
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(192, 2)
     for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
     mbar_init(BAR(kBarSFree), 128);
     mbar_init(BAR(kBarPFull), 128);
+    for (int b = 0; b < 2; ++b) mbar_init(BAR(kBarQFree + b), 128);  // O staged by every softmax thread
     for (int k = 0; k < Cfg::kRing; ++k) mbar_init(BAR(kBarItemFree + k), 5);  // MMA warp + 4 softmax warps
     fence_mbar_init();
   }
@@ -146,8 +151,27 @@ __global__ void __launch_bounds__(192, 2)
       tma_prefetch_desc(&tmO);
     }
     __syncwarp();
+    // The producer also issues the O stores: item m's O is staged in its Q buffer (m & 1) by the
+    // softmax warpgroup, which arrives QFree and moves on; the store is issued here right before
+    // that buffer is refilled with Q(m + 2) (or at the end), keeping the store issue and its
+    // read latency off the softmax warpgroup.
+    Item pend0, pend1;  // by Q buffer (no dynamically indexed array: it would live in local memory)
+    auto store_o = [&](int m) {
+      const int b = m & 1;
+      mbar_wait(BAR(kBarQFree + b), static_cast<uint32_t>((m >> 1) & 1));
+      if constexpr (!OUT_F32) {
+        if (lane == 0) {
+          const Item& pi = b ? pend1 : pend0;
+          tma_store_4d(&tmO, sQ + b * Cfg::kTileBytes, 0, pi.q0, pi.h, pi.b);
+          bulk_commit();
+          bulk_wait_read_all();  // staging read: the buffer may be refilled
+        }
+        __syncwarp();
+      }
+    };
     int g = 0;  // K/V tiles loaded so far (ring position)
-    for (int n = 0;; ++n) {
+    int n = 0;
+    for (;; ++n) {
       if (n >= Cfg::kRing)
         mbar_wait(BAR(kBarItemFree + n % Cfg::kRing), static_cast<uint32_t>((n / Cfg::kRing - 1) & 1));
       int w = -1;
@@ -174,7 +198,9 @@ __global__ void __launch_bounds__(192, 2)
       if (w < 0) break;
       const Item it = item(w, n);
       const int qb = n & 1;
-      if (n >= 2) mbar_wait(BAR(kBarQFree + qb), static_cast<uint32_t>(((n >> 1) - 1) & 1));
+      if (n >= 2) store_o(n - 2);
+      if (qb) pend1 = it;
+      else pend0 = it;
       if (elect_one_sync()) {
         mbar_expect_tx(BAR(kBarQFull + qb), Cfg::kTileBytes);
         tma_load_4d(sQ + qb * Cfg::kTileBytes, &tmQ, BAR(kBarQFull + qb), 0, it.q0, it.h, it.b);
@@ -197,6 +223,8 @@ __global__ void __launch_bounds__(192, 2)
         __syncwarp();
       }
     }
+    for (int m = max(n - 2, 0); m < n; ++m) store_o(m);
+    if (lane == 0) bulk_wait_all();
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer: one global tile stream
     constexpr uint32_t ab = BF16 ? 1u : 0u;
@@ -318,10 +346,12 @@ __global__ void __launch_bounds__(192, 2)
     const bool custom_on = p.custom != nullptr;
     int g = 0;   // global tile index
     int nf = 0;  // OFinal phases consumed (items with tiles)
-    for (int n = 0;; ++n) {
-      const int w = take_item(n);
-      if (w < 0) break;
-      const Item it = item(w, n);
+    // the next item is taken (and decoded) under the current item's last PV, ahead of its epilogue
+    int w_next = take_item(0);
+    Item it_next = item(max(w_next, 0), 0);
+    for (int n = 0; w_next >= 0; ++n) {
+      if (threadIdx.x == 0) TATN_EV(g, 5);
+      const Item it = it_next;
       const int qb = n & 1;
       const int grow = it.q0 + row;
       const int growc = grow - p.k_off;
@@ -373,20 +403,29 @@ __global__ void __launch_bounds__(192, 2)
         }
         auto step = [&](auto masked_t) {
           constexpr bool kMasked = decltype(masked_t)::value;
+          // Masked tiles: `lim` grows with the row, so 32-column chunks at or past the warp's
+          // last row's limit are masked for all 32 rows — warp-uniformly skipped (P = 0, no
+          // exponentials): on a causal diagonal tile warp w computes w + 1 chunks, not 4.
+          int hi = 4;  // chunks [hi, 4) are all-masked for this warp
+          if constexpr (kMasked && TATN_FWD1_CHUNK_SKIP) {
+            hi = (max(__shfl_sync(0xffffffffu, lim, 31), 0) + 31) >> 5;
+          }
           if constexpr (kMasked) {
 #pragma unroll
             for (int c = 0; c < 4; ++c)
+              if (c < hi)
 #pragma unroll
-              for (int i = 0; i < 32; ++i) sv[c][i] = (c * 32 + i >= lim) ? __float_as_uint(-INFINITY) : sv[c][i];
+                for (int i = 0; i < 32; ++i) sv[c][i] = (c * 32 + i >= lim) ? __float_as_uint(-INFINITY) : sv[c][i];
           }
           float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
+            if (!kMasked || c < hi)
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              mx0 = fmax3(mx0, __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
-              mx1 = fmax3(mx1, __uint_as_float(sv[c][i + 2]), __uint_as_float(sv[c][i + 3]));
-            }
+              for (int i = 0; i < 32; i += 4) {
+                mx0 = fmax3(mx0, __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
+                mx1 = fmax3(mx1, __uint_as_float(sv[c][i + 2]), __uint_as_float(sv[c][i + 3]));
+              }
           const float m_tile = fmaxf(mx0, mx1) * sl2;
           const bool jump = m_tile - m_run > kRescaleThreshold;  // false when both are -inf
           if (__any_sync(0xffffffffu, jump)) {                   // warp-uniform: TMEM ld/st are .sync.aligned
@@ -415,6 +454,10 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t pk[16];
+            if (kMasked && c >= hi) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) pk[k] = 0u;
+            } else
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
               const int i = c * 16 + k;
@@ -454,12 +497,15 @@ __global__ void __launch_bounds__(192, 2)
         mbar_arrive(BAR(kBarPFull));
         if (threadIdx.x == 0) TATN_EV(g, 2);
       }
+      w_next = take_item(n + 1);
+      if (w_next >= 0) it_next = item(w_next, n + 1);
       // ---------------- epilogue of item n: O / l -> staging in Q buffer qb -> TMA store; LSE
       mbar_wait(BAR(kBarQFull + qb), static_cast<uint32_t>((n >> 1) & 1));  // Q landed (and is not in flight)
       if (n_done > 0) {
         mbar_wait(BAR(kBarOFinal), static_cast<uint32_t>(nf & 1));  // every MMA of the item done
         ++nf;
         tc_fence_after();
+        if (threadIdx.x == 0) TATN_EV(g - 1, 6);
       }
       const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
       const uint32_t sO = sQ + qb * Cfg::kTileBytes;
@@ -467,15 +513,21 @@ __global__ void __launch_bounds__(192, 2)
       if constexpr (OUT_F32)
         orow = p.o_f32 + static_cast<size_t>(it.b) * p.o_sb + static_cast<size_t>(it.h) * p.o_sh +
                static_cast<size_t>(grow) * p.o_sn;
+      uint32_t oall[D / 32][32];
+      if (n_done > 0) {  // both loads in flight before the first wait
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) tmem_ld32_async(tO + c * 32, oall[c]);
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) tmem_ld_wait32(oall[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) oall[c][i] = 0u;
+      }
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        if (n_done > 0) {
-          tmem_ld32(tO + c * 32, o);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = 0u;
-        }
+        uint32_t* o = oall[c];
         if constexpr (OUT_F32) {
           if (grow < p.Nq) {
 #pragma unroll
@@ -503,17 +555,9 @@ __global__ void __launch_bounds__(192, 2)
       }
       tc_fence_before();  // O read out of TMEM before the next item's first PV (ordered by PFull)
       if constexpr (!OUT_F32) fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (row == 0) {
-        if constexpr (!OUT_F32) {
-          tma_store_4d(&tmO, sO, 0, it.q0, it.h, it.b);
-          bulk_commit();
-          bulk_wait_read_all();  // staging read: the Q buffer may be refilled
-        }
-        mbar_arrive(BAR(kBarQFree + qb));
-      }
+      if (threadIdx.x == 0 && n_done > 0) TATN_EV(g - 1, 7);
+      mbar_arrive(BAR(kBarQFree + qb));  // O staged: the producer issues the store
     }
-    if (row == 0) bulk_wait_all();
   }
 
   tc_fence_before();

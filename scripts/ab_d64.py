@@ -1,0 +1,32 @@
+"""A/B forward+backward timing (graph replays, L2 flushed) of the product library vs variants on
+the d=64 workloads, interleaved subprocess runs: python scripts/ab_d64.py VARIANT... [REPS]."""
+import os, subprocess, sys
+args = [a for a in sys.argv[1:] if not a.isdigit()]
+reps = int(next((a for a in sys.argv[1:] if a.isdigit()), "3"))
+libs = ["product"] + args
+code = r'''
+import sys, torch, json
+sys.path.insert(0, ".")
+import bench
+res = {}
+flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush = lambda: flush_buf.zero_()
+for name in ["gpt2-small", "bert-large", "long-8k-d64", "butterfly-16k"]:
+    w = bench.WORKLOADS[name]
+    q, k, v, do, spec = bench.make_inputs(w, torch.device("cuda"))
+    st = bench.Step(q, k, v, do, spec)
+    f = bench.flops(w)
+    fw = bench.timed(bench.graphed(st.fwd), 20, flush) / 20
+    bw = bench.timed(bench.graphed(st.bwd), 20, flush) / 20
+    res[name] = (round(f[0] / fw / 1e9), round(f[1] / bw / 1e9))
+    del q, k, v, do, st
+    torch.cuda.empty_cache()
+print(json.dumps(res))
+'''
+for rep in range(reps):
+    for lib in libs:
+        env = dict(os.environ)
+        if lib != "product":
+            env["TATN_B200_LIB"] = os.path.abspath(f"paper_2205_14135_b200/lib/variants/lib_{lib}.so")
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        print(f"{lib:>10}", out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-500:], flush=True)

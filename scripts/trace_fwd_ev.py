@@ -5,7 +5,7 @@ sys.path.insert(0, ".")
 os.environ.setdefault("TATN_B200_LIB", os.path.abspath("paper_2205_14135_b200/lib/variants/lib_trace.so"))
 from paper_2205_14135_b200 import attention as A, _lib
 lib = _lib.load()
-names = ["S_seen", "S_free", "P_arrive", "MMA_sawP", "QKnext_iss", "V_full"]
+names = ["S_seen", "S_free", "P_arrive", "MMA_sawP", "QKnext_iss", "item_seen", "OFinal", "O_staged"]
 for (B, H, N, d, mask) in [(8, 12, 1024, 64, "causal"), (2, 32, 8192, 64, "none")]:
     q = torch.randn(B, H, N, d, device="cuda", dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
     spec = A.AttnSpec(mask=mask)
@@ -16,7 +16,7 @@ for (B, H, N, d, mask) in [(8, 12, 1024, 64, "causal"), (2, 32, 8192, 64, "none"
     torch.cuda.synchronize()
     A.flash_fwd(q, k, v, spec); torch.cuda.synchronize()
     lib.tatn_debug_set_trace(ctypes.c_void_p(0))
-    ev = buf[200000 * 16:].view(1024, 8).cpu().numpy().astype(np.int64)[:, :6]
+    ev = buf[200000 * 16:].view(1024, 8).cpu().numpy().astype(np.int64)[:, :8]
     n = int((ev[:, 2] > 0).sum())
     ev = ev[:n]
     t0 = ev[ev > 0].min()
