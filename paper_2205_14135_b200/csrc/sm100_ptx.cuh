@@ -47,6 +47,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Programmatic dependent launch (kernels launched with the PDL attribute, tatn_launch.h): every
+// kernel runs griddep_wait() before its first global-memory access, so its prologue (barrier
+// init, TMEM allocation, descriptor prefetch) overlaps the previous kernel's tail; it signals
+// griddep_launch() once it needs no more SM slots (no items left to claim).
+#ifndef TATN_PDL_EARLY
+#define TATN_PDL_EARLY 0  // 1: persistent kernels signal dependents once no items are left (measured slower:
+                          // the waiting dependent CTAs share SMs with the tail)
+#endif
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // monotonic shared-memory progress counters (for waits a lagging consumer may be >= 2 phases
 // behind or ahead of, which an mbarrier parity wait cannot express)
 __device__ __forceinline__ void st_release_u32(uint32_t addr, uint32_t v) {

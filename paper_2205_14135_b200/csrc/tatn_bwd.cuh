@@ -35,6 +35,7 @@
 #include "../../include/tatn_b200.h"
 #include "sm100_ptx.cuh"
 #include "tatn_params.h"
+#include "tatn_launch.h"
 
 #ifndef TATN_BWD_SPLIT
 #define TATN_BWD_SPLIT 0  // softmax warpgroups split each Q tile's columns (1) or alternate tiles (0)
@@ -161,6 +162,8 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_,
                                                     int B, int H, int Nq, int Nq_pad, float* __restrict__ lse2,
                                                     float* __restrict__ delta, float* __restrict__ dq_acc,
                                                     int* __restrict__ item_counter) {
+  griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
+  griddep_launch();
   constexpr int kChunks = D / 8;
   const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long row = gid / kChunks;  // over B*H*Nq_pad
@@ -228,6 +231,8 @@ template <int D, bool BF16, bool OUT_F32>
 __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ dq_acc, void* __restrict__ dq,
                                                      int64_t qb, int64_t qh, int64_t qn, int B, int H, int Nq,
                                                      int Nq_pad) {
+  griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
+  griddep_launch();
   constexpr int kChunks = D / 8;
   const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long row = gid / kChunks;  // over B*H*Nq
@@ -260,6 +265,8 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
 __global__ void __launch_bounds__(256) tatn_custom_transpose(const uint32_t* __restrict__ in, int words, int64_t bstride,
                                                              int nb, int Nq, int Nk, int tw, uint32_t* __restrict__ out,
                                                              int kw_off) {
+  griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
+  griddep_launch();
   const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = static_cast<int>(threadIdx.x & 31);
   const int kwords = (Nk + 31) / 32;
@@ -394,6 +401,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     __syncwarp();
   };
   constexpr bool kSparsePersistent = Cfg::kMaskSlots == kItemRing;
+  griddep_wait();  // K2's outputs (workspace, item counter) are visible from here on
   // d = 128 block-sparse launches run one item per CTA (grid = items)
   if (!kSparsePersistent && p.grid != nullptr && warp == kProducerWarp) build_col_mask(static_cast<int>(blockIdx.x), mask_smem);
   tc_fence_before();
@@ -443,6 +451,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       w = __shfl_sync(0xffffffffu, w, 0);
       if (w >= p.n_items) w = -1;
+      if (w < 0 && TATN_PDL_EARLY) griddep_launch();  // no more items: K4 may take freed SM slots
       if (kSparsePersistent && p.grid != nullptr && w >= 0) build_col_mask(w, mask_smem + (n % kItemRing) * 128);
       if (lane == 0) {
         ring[n % kItemRing] = w;
@@ -981,18 +990,17 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     const int nb = d.custom_bstride != 0 ? d.B : 1;
     const long long warps = static_cast<long long>(nb) * custom_t_words * ((d.Nk + 31) / 32);
     const int blocks = static_cast<int>((warps * 32 + 255) / 256);
-    tatn_dev::tatn_custom_transpose<<<blocks, 256, 0, stream>>>(d.custom_mask, d.custom_words, d.custom_bstride, nb,
-                                                                 d.Nq, d.Nk, custom_t_words, custom_t, d.k_offset / 32);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = tatn_host::launch(tatn_dev::tatn_custom_transpose, dim3(blocks), dim3(256), 0, stream, d.custom_mask,
+                                      d.custom_words, d.custom_bstride, nb, d.Nq, d.Nk, custom_t_words, custom_t,
+                                      d.k_offset / 32);
     if (e != cudaSuccess) return e;
   }
   {
     const long long threads = static_cast<long long>(rows) * (D / 8);
     const int blocks = static_cast<int>((threads + 255) / 256);
-    tatn_dev::tatn_bwd_pre<D, BF16, OUT_F32><<<blocks, 256, 0, stream>>>(
-        o, static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
-        d.H, d.Nq, Nq_pad, lse2, delta, dq_acc, item_counter);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = tatn_host::launch(tatn_dev::tatn_bwd_pre<D, BF16, OUT_F32>, dim3(blocks), dim3(256), 0, stream, o,
+                                      static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
+                                      d.H, d.Nq, Nq_pad, lse2, delta, dq_acc, item_counter);
     if (e != cudaSuccess) return e;
   }
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
@@ -1053,16 +1061,16 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
                                        ? p.n_items
                                        : std::min(p.n_items, n_sm)));
   cudaEvent_t prof_stop = tatn_host::profile_begin(1, stream);
-  kern<<<grid, tatn_dev::kBwdThreads, Cfg::kSmemBytes, stream>>>(mq, mk, mv, mdo, mdk, mdv, p, lse2, Nq_pad);
+  cudaError_t e = tatn_host::launch(kern, grid, dim3(tatn_dev::kBwdThreads), Cfg::kSmemBytes, stream, mq, mk, mv, mdo,
+                                    mdk, mdv, p, static_cast<const float*>(lse2), Nq_pad);
   if (prof_stop) cudaEventRecord(prof_stop, stream);
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   {
     const long long threads = static_cast<long long>(d.B) * d.H * d.Nq * (D / 8);
     const int blocks = static_cast<int>((threads + 255) / 256);
-    tatn_dev::tatn_bwd_post<D, BF16, OUT_F32><<<blocks, 256, 0, stream>>>(dq_acc, dq, d.q_str[0],
-                                                                 d.q_str[1], d.q_str[2], d.B, d.H, d.Nq, Nq_pad);
-    e = cudaGetLastError();
+    e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, BF16, OUT_F32>, dim3(blocks), dim3(256), 0, stream,
+                          static_cast<const float*>(dq_acc), dq, d.q_str[0], d.q_str[1], d.q_str[2], d.B, d.H, d.Nq,
+                          Nq_pad);
     if (e != cudaSuccess) return e;
   }
   *launches = custom ? 4 : 3;

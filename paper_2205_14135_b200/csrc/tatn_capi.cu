@@ -195,8 +195,7 @@ cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   if (ctr == nullptr) return cudaErrorInvalidValue;
   // persistent: two CTAs per SM
   const int grid = std::min(pp.n_items, 2 * tatn_host::sm_count());
-  kern<<<grid, 192, Cfg::kSmemBytes, stream>>>(q, k, v, o, pp, ctr);
-  return cudaGetLastError();
+  return tatn_host::launch(kern, dim3(grid), dim3(192), Cfg::kSmemBytes, stream, q, k, v, o, pp, ctr);
 }
 
 template <bool BF16, bool OUT_F32, bool DROP>
@@ -217,8 +216,7 @@ cudaError_t launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   int* ctr = fwd_counter();
   if (ctr == nullptr) return cudaErrorInvalidValue;
   const int grid = std::min(pp.n_items, tatn_host::sm_count());  // persistent, one CTA per SM
-  kern<<<grid, 384, Cfg::kSmemBytes, stream>>>(q, k, v, pp, ctr);
-  return cudaGetLastError();
+  return tatn_host::launch(kern, dim3(grid), dim3(384), Cfg::kSmemBytes, stream, q, k, v, pp, ctr);
 }
 
 template <int D, bool BF16, bool OUT_F32, bool DROP, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
@@ -241,8 +239,7 @@ cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
     pp.n_pairs = (p.Nq + 128 * NQ - 1) / (128 * NQ);  // Q-tile groups (of NQ tiles) per head
     pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * D * 4.0, NQ == 2 ? 1 : 2);
     dim3 grid(static_cast<unsigned>(p.B * p.H * pp.n_pairs));
-    kern<<<grid, tatn_dev::fwd_threads<NQ>(), Cfg::kSmemBytes, stream>>>(q, k, v, o, pp);
-    return cudaGetLastError();
+    return tatn_host::launch(kern, grid, dim3(tatn_dev::fwd_threads<NQ>()), Cfg::kSmemBytes, stream, q, k, v, o, pp);
   }
 }
 
@@ -293,9 +290,10 @@ int tatn_merge_partials(int32_t R, int32_t B, int32_t H, int32_t Nq, int32_t d, 
   const long long rows = static_cast<long long>(B) * H * Nq;
   const long long threads = rows * (d / 8);
   const int blocks = static_cast<int>((threads + 255) / 256);
-  tatn_dev::tatn_merge_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      R, rows, d, H, Nq, o_parts, lse_parts, o, o_dtype, o_str[0], o_str[1], o_str[2], lse);
-  if (cudaGetLastError() != cudaSuccess) return TATN_E_CUDA;
+  if (tatn_host::launch(tatn_dev::tatn_merge_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), R,
+                        rows, d, H, Nq, o_parts, lse_parts, o, o_dtype, o_str[0], o_str[1], o_str[2],
+                        lse) != cudaSuccess)
+    return TATN_E_CUDA;
   g_last_launches = 1;
   return TATN_OK;
 }

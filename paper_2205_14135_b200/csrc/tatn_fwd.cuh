@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
         if (lane == 0) mask_smem[q * (kMaxSparseTiles / 32) + (base >> 5)] = bits;
       }
   }
+  griddep_wait();  // the previous kernel's outputs are visible from here on
+  griddep_launch();  // one item per CTA: dependents may fill slots of finished CTAs
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -897,6 +899,8 @@ __global__ void __launch_bounds__(256) tatn_merge_kernel(int R, long long rows, 
                                                          const float* __restrict__ lse_parts, void* __restrict__ o,
                                                          int o_dtype, int64_t ob, int64_t oh, int64_t on,
                                                          float* __restrict__ lse) {
+  griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
+  griddep_launch();
   const int chunks = d / 8;
   const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long row = gid / chunks;

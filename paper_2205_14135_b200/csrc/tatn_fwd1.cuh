@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(192, 2)
     tmem_alloc(smem_u32(tmem_slot), Cfg::kTmemCols);
     tmem_relinquish();
   }
+  griddep_wait();  // the previous kernel's outputs are visible from here on
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(192, 2)
       if (lane == 0) w = atomicAdd(ctr, 1);
       w = __shfl_sync(0xffffffffu, w, 0);
       if (w >= p.n_items) w = -1;
+      if (w < 0 && TATN_PDL_EARLY) griddep_launch();  // no more items: the next kernel may take freed SM slots
       if (sparse && w >= 0) {  // the item's grid row -> bitmask slot n % kRing (read once, coalesced)
         int bh0, qt0;
         fwd1_item(p, w, bh0, qt0);

@@ -1,4 +1,4 @@
-"""A/B forward+backward timing (graph replays, L2 flushed) of the product library vs variants on
+"""A/B forward+backward timing (variants: lib/variants/lib_NAME.so, or VAR=VALUE env settings) (graph replays, L2 flushed) of the product library vs variants on
 the d=64 workloads, interleaved subprocess runs: python scripts/ab_d64.py VARIANT... [REPS]."""
 import os, subprocess, sys
 args = [a for a in sys.argv[1:] if not a.isdigit()]
@@ -11,7 +11,8 @@ import bench
 res = {}
 flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 flush = lambda: flush_buf.zero_()
-for name in ["gpt2-small", "bert-large", "long-8k-d64", "butterfly-16k"]:
+import os
+for name in os.environ.get("AB_WORKLOADS", "gpt2-small,bert-large,long-8k-d64,butterfly-16k").split(","):
     w = bench.WORKLOADS[name]
     q, k, v, do, spec = bench.make_inputs(w, torch.device("cuda"))
     st = bench.Step(q, k, v, do, spec)
@@ -26,7 +27,10 @@ print(json.dumps(res))
 for rep in range(reps):
     for lib in libs:
         env = dict(os.environ)
-        if lib != "product":
+        if "=" in lib:  # product library with an environment setting, e.g. TATN_PDL=0
+            k_, v_ = lib.split("=", 1)
+            env[k_] = v_
+        elif lib != "product":
             env["TATN_B200_LIB"] = os.path.abspath(f"paper_2205_14135_b200/lib/variants/lib_{lib}.so")
         out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         print(f"{lib:>10}", out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-500:], flush=True)
