@@ -63,7 +63,7 @@ typedef enum {
 } tatn_mask_kind;
 
 typedef struct {
-  int32_t B, H;      /* independent (batch, head) slices                          */
+  int32_t B, H;      /* independent (batch, head) slices, each 1..65535           */
   int32_t Nq, Nk;    /* query rows, key rows (Nk <= Nq: key prefix, reference.hpp:43-46) */
   int32_t d;         /* head dimension: 64 or 128                                 */
   int32_t dtype;     /* tatn_dtype of q, k, v, dO                                 */

@@ -155,7 +155,9 @@ __device__ __forceinline__ BwdSched make_bwd_sched(const BwdParams& p, int b, in
 }
 
 // ---------------------------------------------------------------- K2
-// One 8-element chunk per thread. Rows are padded to a multiple of 128.
+// One 8-element chunk per thread; grid (row blocks, H, B) so no thread divides 64-bit indices
+// (the divisions cost as much issue time as the bytes these HBM-bound kernels move). Rows are
+// padded to a multiple of 128.
 template <int D, bool BF16, bool O_F32>
 __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_, const uint16_t* __restrict__ dO,
                                                     const float* __restrict__ lse, int64_t ob, int64_t oh, int64_t on,
@@ -165,18 +167,16 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_,
   griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
   griddep_launch();
   constexpr int kChunks = D / 8;
-  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long row = gid / kChunks;  // over B*H*Nq_pad
-  const int c = static_cast<int>(gid % kChunks);
-  const long long total = static_cast<long long>(B) * H * Nq_pad;
-  if (gid == 0) *item_counter = 0;  // K3's persistent scheduler starts from item 0
+  constexpr int kRowsPerBlock = 256 / kChunks;
+  const int c = static_cast<int>(threadIdx.x) % kChunks;
+  const int qi = static_cast<int>(blockIdx.x) * kRowsPerBlock + static_cast<int>(threadIdx.x) / kChunks;
+  const int h = static_cast<int>(blockIdx.y), b = static_cast<int>(blockIdx.z);
+  const long long bh = static_cast<long long>(b) * H + h;
+  const long long row = bh * Nq_pad + qi;  // over B*H*Nq_pad
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
+    *item_counter = 0;  // K3's persistent scheduler starts from item 0
   float part = 0.f;
-  int qi = 0;
-  long long bh = 0;
-  if (row < total) {
-    bh = row / Nq_pad;
-    qi = static_cast<int>(row - bh * Nq_pad);
-    const int b = static_cast<int>(bh / H), h = static_cast<int>(bh % H);
+  if (qi < Nq_pad) {
     if (qi < Nq) {
       const size_t off = static_cast<size_t>(b) * ob + static_cast<size_t>(h) * oh + static_cast<size_t>(qi) * on + c * 8;
       const uint4 dv = *reinterpret_cast<const uint4*>(dO + off);
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_,
   // reduce over the kChunks lanes of this row (kChunks in {8, 16}, aligned within a warp)
 #pragma unroll
   for (int off = kChunks / 2; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-  if (row < total && c == 0) {
+  if (qi < Nq_pad && c == 0) {
     delta[row] = -part;    // stored negated: the softmax step adds it
     float nl2 = -INFINITY;  // P = 0 for padded or fully-masked rows
     if (qi < Nq) {
@@ -234,13 +234,12 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
   griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
   griddep_launch();
   constexpr int kChunks = D / 8;
-  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long row = gid / kChunks;  // over B*H*Nq
-  const int c = static_cast<int>(gid % kChunks);
-  if (row >= static_cast<long long>(B) * H * Nq) return;
-  const long long bh = row / Nq;
-  const int qi = static_cast<int>(row - bh * Nq);
-  const int b = static_cast<int>(bh / H), h = static_cast<int>(bh % H);
+  constexpr int kRowsPerBlock = 256 / kChunks;
+  const int c = static_cast<int>(threadIdx.x) % kChunks;
+  const int qi = static_cast<int>(blockIdx.x) * kRowsPerBlock + static_cast<int>(threadIdx.x) / kChunks;
+  const int h = static_cast<int>(blockIdx.y), b = static_cast<int>(blockIdx.z);
+  const long long bh = static_cast<long long>(b) * H + h;
+  if (qi >= Nq) return;
   const float4* src = reinterpret_cast<const float4*>(dq_acc + (bh * Nq_pad + qi) * D + c * 8);
   const float4 a = src[0], bb = src[1];
   const size_t off = static_cast<size_t>(b) * qb + static_cast<size_t>(h) * qh + static_cast<size_t>(qi) * qn + c * 8;
@@ -996,9 +995,8 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
     if (e != cudaSuccess) return e;
   }
   {
-    const long long threads = static_cast<long long>(rows) * (D / 8);
-    const int blocks = static_cast<int>((threads + 255) / 256);
-    cudaError_t e = tatn_host::launch(tatn_dev::tatn_bwd_pre<D, BF16, OUT_F32>, dim3(blocks), dim3(256), 0, stream, o,
+    const dim3 blocks(static_cast<unsigned>((Nq_pad + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
+    cudaError_t e = tatn_host::launch(tatn_dev::tatn_bwd_pre<D, BF16, OUT_F32>, blocks, dim3(256), 0, stream, o,
                                       static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
                                       d.H, d.Nq, Nq_pad, lse2, delta, dq_acc, item_counter);
     if (e != cudaSuccess) return e;
@@ -1066,9 +1064,8 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   if (prof_stop) cudaEventRecord(prof_stop, stream);
   if (e != cudaSuccess) return e;
   {
-    const long long threads = static_cast<long long>(d.B) * d.H * d.Nq * (D / 8);
-    const int blocks = static_cast<int>((threads + 255) / 256);
-    e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, BF16, OUT_F32>, dim3(blocks), dim3(256), 0, stream,
+    const dim3 blocks(static_cast<unsigned>((d.Nq + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
+    e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, BF16, OUT_F32>, blocks, dim3(256), 0, stream,
                           static_cast<const float*>(dq_acc), dq, d.q_str[0], d.q_str[1], d.q_str[2], d.B, d.H, d.Nq,
                           Nq_pad);
     if (e != cudaSuccess) return e;

@@ -125,6 +125,7 @@ bool strides_ok(const int64_t s[3], int H, int N, int d) {
 int validate(const tatn_attn_desc* d) {
   if (d == nullptr) return TATN_E_ARG;
   if (d->B < 1 || d->H < 1 || d->Nq < 1 || d->Nk < 1) return TATN_E_SHAPE;
+  if (d->B > 65535 || d->H > 65535) return TATN_E_SHAPE;  // K2 / K4 grid (rows, H, B)
   if (d->Nk > d->Nq) return TATN_E_SHAPE;  // more keys than n (reference.cpp:25-26)
   if (d->d != 64 && d->d != 128) return TATN_E_UNSUPPORTED;
   if (d->dtype != TATN_DTYPE_BF16 && d->dtype != TATN_DTYPE_FP16) return TATN_E_UNSUPPORTED;
@@ -171,6 +172,9 @@ CUtensorMapDataType tma_dtype(int dtype) {
 #ifndef TATN_FWD_PERSISTENT
 #define TATN_FWD_PERSISTENT 1  // d = 64: persistent kernel (tatn_fwd1.cuh)
 #endif
+#ifndef TATN_FWD_D64_PAIRS
+#define TATN_FWD_D64_PAIRS 0  // experiment: d = 64 on the Q-tile-pair kernel (tatn_fwd2.cuh)
+#endif
 #ifndef TATN_FWD2_PERSISTENT
 #define TATN_FWD2_PERSISTENT 1  // d = 128: persistent kernel (tatn_fwd2.cuh)
 #endif
@@ -198,11 +202,11 @@ cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   return tatn_host::launch(kern, dim3(grid), dim3(192), Cfg::kSmemBytes, stream, q, k, v, o, pp, ctr);
 }
 
-template <bool BF16, bool OUT_F32, bool DROP>
+template <int D, bool BF16, bool OUT_F32, bool DROP>
 cudaError_t launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                         const tatn_dev::FwdParams& p, cudaStream_t stream) {
-  using Cfg = tatn_dev::Fwd2Cfg<128>;
-  auto kern = tatn_dev::tatn_fwd2_kernel<128, BF16, OUT_F32, DROP>;
+  using Cfg = tatn_dev::Fwd2Cfg<D>;
+  auto kern = tatn_dev::tatn_fwd2_kernel<D, BF16, OUT_F32, DROP>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -212,7 +216,7 @@ cudaError_t launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   tatn_dev::FwdParams pp = p;
   pp.n_pairs = (p.Nq + 255) / 256;  // Q-tile pairs per (b, h)
   pp.n_items = p.B * p.H * pp.n_pairs;
-  pp.group = schedule_group(p.B * p.H, 1, static_cast<double>(p.Nk) * 128 * 4.0, 1);
+  pp.group = schedule_group(p.B * p.H, 1, static_cast<double>(p.Nk) * D * 4.0, 1);
   int* ctr = fwd_counter();
   if (ctr == nullptr) return cudaErrorInvalidValue;
   const int grid = std::min(pp.n_items, tatn_host::sm_count());  // persistent, one CTA per SM
@@ -222,10 +226,12 @@ cudaError_t launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtens
 template <int D, bool BF16, bool OUT_F32, bool DROP, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
 cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
-  if constexpr (D == 64 && TATN_FWD_PERSISTENT) {
+  if constexpr (D == 64 && TATN_FWD_D64_PAIRS) {
+    return launch_fwd2<64, BF16, OUT_F32, DROP>(q, k, v, p, stream);
+  } else if constexpr (D == 64 && TATN_FWD_PERSISTENT) {
     return launch_fwd1<BF16, OUT_F32, DROP>(q, k, v, o, p, stream);
   } else if constexpr (D == 128 && TATN_FWD2_PERSISTENT) {
-    return launch_fwd2<BF16, OUT_F32, DROP>(q, k, v, p, stream);
+    return launch_fwd2<128, BF16, OUT_F32, DROP>(q, k, v, p, stream);
   } else {
     using Cfg = tatn_dev::FwdCfg<D, NQ>;
     auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ, DROP>;

@@ -74,6 +74,8 @@ def test_valid_descriptor_passes():
     [
         (dict(B=0), _lib.TATN_E_SHAPE),
         (dict(Nq=0), _lib.TATN_E_SHAPE),
+        (dict(H=65536), _lib.TATN_E_SHAPE),  # K2 / K4 grid dimension (rows, H, B)
+        (dict(B=65536), _lib.TATN_E_SHAPE),
         (dict(Nk=301), _lib.TATN_E_SHAPE),  # more keys than n (reference.cpp:25-26)
         (dict(d=32), _lib.TATN_E_UNSUPPORTED),
         (dict(dtype=7), _lib.TATN_E_UNSUPPORTED),
