@@ -40,6 +40,9 @@
 #ifndef TATN_BWD_SPLIT
 #define TATN_BWD_SPLIT 0  // softmax warpgroups split each Q tile's columns (1) or alternate tiles (0)
 #endif
+#ifndef TATN_BWD_DS_BUFS
+#define TATN_BWD_DS_BUFS 2  // d = 64 dS^T buffers (3 measured no faster: the softmax is not waiting on them)
+#endif
 #ifndef TATN_DQ_RED
 #define TATN_DQ_RED 1  // dQ partials: red.global.add from registers (1) or smem staging + bulk reduce (0)
 #endif
@@ -63,6 +66,10 @@ struct BwdCfg {
   // d = 128 with dropout drops to 2 stages to make room for the per-warpgroup row hashes
   static constexpr int kStages = (D == 128) ? (DROP ? 2 : 3) : 4;
   static constexpr int kDSBytes = 128 * 128;          // 128 keys x 64 q x 2B
+  // dS^T shared-memory buffers (tile g uses g % kDSBufs): with 3 at d = 64 the softmax of tile
+  // g waits for the dQ^T MMA of tile g - 3, not g - 2 (issued after the front of tile g)
+  static constexpr int kDSBufs = (D == 64) ? TATN_BWD_DS_BUFS : 2;
+  static_assert(kDSBufs >= 2, "the ping-pong needs two dS^T buffers");
   static constexpr int kDQBytes = kBwdQT * D * 4;     // fp32 staging
   static constexpr int kVecBytes = 2 * kBwdQT * 4;    // lse2 + D
   // K/V buffers: double-buffered at d = 64 (the next item's K/V lands while this one runs)
@@ -71,7 +78,7 @@ struct BwdCfg {
   static constexpr int kOffQ = kOffKV + kKVBufs * 2 * kKVTile;
   static constexpr int kOffDO = kOffQ + kStages * kQTile;
   static constexpr int kOffDS = kOffDO + kStages * kQTile;
-  static constexpr int kOffDQ = kOffDS + 2 * kDSBytes;
+  static constexpr int kOffDQ = kOffDS + kDSBufs * kDSBytes;
   static constexpr int kOffVec = kOffDQ + kDQBytes;
   static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
   static constexpr int kOffRing = kOffBar + 384;       // item ring (kItemRing ints)
@@ -334,8 +341,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int kBarPFull = kBarSFull + 2;      // [2]
   const int kBarDQFull = kBarPFull + 2;     // [2]
   const int kBarDQEmpty = kBarDQFull + 2;   // [2]
-  const int kBarDSEmpty = kBarDQEmpty + 2;  // [2]
-  const int kBarKVFull = kBarDSEmpty + 2;   // [NKV]
+  const int kBarDSEmpty = kBarDQEmpty + 2;  // [kDSBufs]
+  const int kBarKVFull = kBarDSEmpty + Cfg::kDSBufs;  // [NKV]
   const int kBarKVFree = kBarKVFull + NKV;  // [NKV] MMAs of the buffer's item done
   const int kBarFinal = kBarKVFree + NKV;   // item's MMAs done (dK, dV final in TMEM)
   const int kBarAccFree = kBarFinal + 1;    // dK / dV drained from TMEM (count 128)
@@ -345,7 +352,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int kBarItem = kBarStageFree + 1;   // [kItemRing] item id published
   const int kBarItemFree = kBarItem + kItemRing;  // [kItemRing] slot read by all 13 consumer warps
   const int kNumBars = kBarItemFree + kItemRing;
-  static_assert(8 * (2 * S + 10 + 2 * NKV + 3 + 2 * kItemRing) <= 8 * 46, "barrier region");
+  static_assert(8 * (2 * S + 8 + Cfg::kDSBufs + 2 * NKV + 3 + 2 * kItemRing) <= 8 * 46, "barrier region");
   volatile int* ring = reinterpret_cast<volatile int*>(smem_gen + Cfg::kOffRing);
   // Dense launches are persistent (one CTA per SM): the producer claims items from a
   // global counter (zeroed by K2) and publishes them; block-sparse launches run exactly
@@ -611,11 +618,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (elect_one_sync()) {
 #pragma unroll
             for (int kk = 0; kk < kBwdKT / 16; ++kk)
-              mma_ss(tDQ, dKmn0 + ((koff + kk * 2048) >> 4), dDS0 + ((x * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq,
+              mma_ss(tDQ, dKmn0 + ((koff + kk * 2048) >> 4), dDS0 + (((g % Cfg::kDSBufs) * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq,
                      kk > 0 ? 1u : 0u);
             mma_commit(BAR(kBarDQFull + x));
             mma_commit(BAR(kBarQEmpty + s));
-            mma_commit(BAR(kBarDSEmpty + x));
+            mma_commit(BAR(kBarDSEmpty + g % Cfg::kDSBufs));
           }
           __syncwarp();
           if (lane == 0) TATN_EV(g, 4);
@@ -712,7 +719,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld32_async(tX + 64 + 32 * hbase, dp);
         tmem_ld_wait32(sr);
         tmem_ld_wait32(dp);
-        const uint32_t drow = sDS + x * Cfg::kDSBytes + r * 128;
+        const int xs = g % Cfg::kDSBufs;  // dS^T buffer
+        const uint32_t drow = sDS + xs * Cfg::kDSBytes + r * 128;
         auto body = [&](auto masked_t) {
           constexpr bool kMasked = decltype(masked_t)::value;
 #pragma unroll
@@ -772,9 +780,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             if (hh == 0) {
               // the dQ^T MMA of tile g - 2 must have released the dS^T buffer, and in a new
               // item the previous item's dK / dV staging must have been stored
-              mbar_wait(BAR(kBarDSEmpty + x), static_cast<uint32_t>(((g >> 1) & 1) ^ 1));
+              mbar_wait(BAR(kBarDSEmpty + xs), static_cast<uint32_t>(((g / Cfg::kDSBufs) & 1) ^ 1));
               if (first) wait_counter_ge(BAR(kBarStageFree), static_cast<uint32_t>(n));
               first = false;
+              if (D == 64 && r == 0) TATN_EV(g, 6);
             }
             // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
 #pragma unroll

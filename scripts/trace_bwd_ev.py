@@ -5,7 +5,7 @@ sys.path.insert(0, ".")
 os.environ.setdefault("TATN_B200_LIB", os.path.abspath("paper_2205_14135_b200/lib/variants/lib_trace.so"))
 from paper_2205_14135_b200 import attention as A, _lib
 lib = _lib.load()
-names = ["S_seen", "P_arrive", "MMA_sawP", "front_s_issued", "dq_issued", "dQ_seen", "reduce", "QFull_seen"]
+names = ["S_seen", "P_arrive", "MMA_sawP", "front_s_issued", "dq_issued", "dQ_seen", "reduce|dsfree", "QFull_seen"]
 for (B, H, N, d, mask) in [(8, 12, 1024, 64, "causal"), (1, 32, 4096, 128, "causal")]:
     q = torch.randn(B, H, N, d, device="cuda", dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
     do = torch.randn_like(q)

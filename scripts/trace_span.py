@@ -28,3 +28,4 @@ for which in ("fwd", "bwd"):
         busy = (end - start) / 1e3
         print(f"{which} B{B} H{H} N{N} d{d} {mask}: {len(t)} CTAs, events {e0.elapsed_time(e1)*1e3:.1f} us, CTA span {span:.1f} us;"
               f" start offsets max {(start.max()-t0)/1e3:.1f} us; busy mean {busy.mean():.1f} min {busy.min():.1f} max {busy.max():.1f} us")
+        print("   end deciles (us):", " ".join(f"{x:.1f}" for x in np.percentile((end - t0) / 1e3, [0, 10, 50, 90, 100])))
