@@ -719,6 +719,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld32_async(tX + 64 + 32 * hbase, dp);
         tmem_ld_wait32(sr);
         tmem_ld_wait32(dp);
+        if (D == 64 && r == 0) TATN_EV(g, 6);
         const int xs = g % Cfg::kDSBufs;  // dS^T buffer
         const uint32_t drow = sDS + xs * Cfg::kDSBytes + r * 128;
         auto body = [&](auto masked_t) {
@@ -783,7 +784,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               mbar_wait(BAR(kBarDSEmpty + xs), static_cast<uint32_t>(((g / Cfg::kDSBufs) & 1) ^ 1));
               if (first) wait_counter_ge(BAR(kBarStageFree), static_cast<uint32_t>(n));
               first = false;
-              if (D == 64 && r == 0) TATN_EV(g, 6);
             }
             // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
 #pragma unroll

@@ -293,10 +293,11 @@ int tatn_merge_partials(int32_t R, int32_t B, int32_t H, int32_t Nq, int32_t d, 
   if (o_dtype != TATN_DTYPE_BF16 && o_dtype != TATN_DTYPE_FP16 && o_dtype != TATN_DTYPE_FP32) return TATN_E_ARG;
   for (int i = 0; i < 3; ++i)
     if (o_str[i] <= 0 || (o_str[i] % 8) != 0) return TATN_E_SHAPE;
+  if (B > 65535 || H > 65535) return TATN_E_SHAPE;
   const long long rows = static_cast<long long>(B) * H * Nq;
-  const long long threads = rows * (d / 8);
-  const int blocks = static_cast<int>((threads + 255) / 256);
-  if (tatn_host::launch(tatn_dev::tatn_merge_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), R,
+  const int rows_per_block = 256 / (d / 8);
+  const dim3 blocks(static_cast<unsigned>((Nq + rows_per_block - 1) / rows_per_block), H, B);
+  if (tatn_host::launch(tatn_dev::tatn_merge_kernel, blocks, dim3(256), 0, static_cast<cudaStream_t>(stream), R,
                         rows, d, H, Nq, o_parts, lse_parts, o, o_dtype, o_str[0], o_str[1], o_str[2],
                         lse) != cudaSuccess)
     return TATN_E_CUDA;

@@ -901,11 +901,13 @@ __global__ void __launch_bounds__(256) tatn_merge_kernel(int R, long long rows, 
                                                          float* __restrict__ lse) {
   griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
   griddep_launch();
+  // grid (row blocks, H, B): no per-thread 64-bit index divisions
   const int chunks = d / 8;
-  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long row = gid / chunks;
-  const int c = static_cast<int>(gid - row * chunks);
-  if (row >= rows) return;
+  const int c = static_cast<int>(threadIdx.x) % chunks;
+  const int n = static_cast<int>(blockIdx.x) * (256 / chunks) + static_cast<int>(threadIdx.x) / chunks;
+  const int h = static_cast<int>(blockIdx.y), b = static_cast<int>(blockIdx.z);
+  if (n >= Nq) return;
+  const long long row = (static_cast<long long>(b) * H + h) * Nq + n;
   float m = -INFINITY;
   for (int r = 0; r < R; ++r) m = fmaxf(m, lse_parts[static_cast<size_t>(r) * rows + row]);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -924,9 +926,7 @@ __global__ void __launch_bounds__(256) tatn_merge_kernel(int R, long long rows, 
     }
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-  const long long bh = row / Nq;
-  const int n = static_cast<int>(row - bh * Nq);
-  const size_t off = static_cast<size_t>(bh / H) * ob + static_cast<size_t>(bh % H) * oh + static_cast<size_t>(n) * on + c * 8;
+  const size_t off = static_cast<size_t>(b) * ob + static_cast<size_t>(h) * oh + static_cast<size_t>(n) * on + c * 8;
   if (o_dtype == 2) {
     float4* dst = reinterpret_cast<float4*>(static_cast<float*>(o) + off);
     dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);

@@ -84,3 +84,35 @@ def test_graph_replay_matches_eager(cuda_device):
     for a, b in zip((o, lse, dk, dv), ref[:4]):
         assert torch.equal(a, b)
     assert torch.allclose(dq.float(), ref[4].float(), atol=2e-2, rtol=0)
+
+
+_PDL_CHILD = r'''
+import sys, torch
+sys.path.insert(0, ".")
+from paper_2205_14135_b200 import attention as A
+g = torch.Generator(device="cuda").manual_seed(11)
+q, k, v, do = (torch.randn((4, 8, 1000, 64), generator=g, device="cuda").half() for _ in range(4))
+spec = A.AttnSpec(mask="causal")
+o, lse = A.flash_fwd(q, k, v, spec)
+dq, dk, dv = A.flash_bwd(q, k, v, o, do, lse, spec)
+torch.save({"o": o.cpu(), "lse": lse.cpu(), "dk": dk.cpu(), "dv": dv.cpu(), "dq": dq.float().cpu()}, sys.argv[1])
+'''
+
+
+def test_programmatic_dependent_launch_matches_plain_launches(tmp_path):
+    """Every kernel is launched with programmatic stream serialization and holds itself at
+    griddepcontrol.wait; TATN_PDL=0 launches plainly. The two must give the same results."""
+    import os
+    import subprocess
+    import sys
+
+    res = {}
+    for pdl in ("1", "0"):
+        out = tmp_path / f"pdl{pdl}.pt"
+        env = dict(os.environ, TATN_PDL=pdl)
+        subprocess.run([sys.executable, "-c", _PDL_CHILD, str(out)], env=env, check=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        res[pdl] = torch.load(out)
+    for key in ("o", "lse", "dk", "dv"):
+        assert torch.equal(res["1"][key], res["0"][key]), key
+    assert torch.allclose(res["1"]["dq"], res["0"]["dq"], atol=2e-2, rtol=0)
