@@ -199,7 +199,8 @@ cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtens
   if (ctr == nullptr) return cudaErrorInvalidValue;
   // persistent: two CTAs per SM
   const int grid = std::min(pp.n_items, 2 * tatn_host::sm_count());
-  return tatn_host::launch(kern, dim3(grid), dim3(192), Cfg::kSmemBytes, stream, q, k, v, o, pp, ctr);
+  return tatn_host::launch(kern, dim3(grid), dim3(tatn_dev::kFwd1Threads), Cfg::kSmemBytes, stream, q, k, v, o, pp,
+                           ctr);
 }
 
 template <int D, bool BF16, bool OUT_F32, bool DROP>

@@ -51,8 +51,13 @@ __device__ __forceinline__ void fwd1_item(const FwdParams& p, int w, int& bh, in
   qt = (p.mask_kind == kMaskCausal && p.grid == nullptr) ? (p.n_pairs - 1 - slot) : slot;
 }
 
+#ifndef TATN_FWD1_WIDE
+#define TATN_FWD1_WIDE 0  // 1: 256 threads (2 idle warps) so setmaxnreg can move registers to the softmax
+#endif
+constexpr int kFwd1Threads = TATN_FWD1_WIDE ? 256 : 192;
+
 template <bool BF16, bool OUT_F32, bool DROP>
-__global__ void __launch_bounds__(192, 2)
+__global__ void __launch_bounds__(kFwd1Threads, 2)
     tatn_fwd1_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                      const FwdParams p, int* __restrict__ ctr) {
@@ -99,6 +104,11 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+#if TATN_FWD1_WIDE
+  // two full warpgroups: softmax 0-3 (setmaxnreg.inc in its branch), producer / MMA / two idle
+  // warps give registers back here
+  if (warp >= 4) setmaxnreg_dec<56>();
+#endif
 
   // per-item schedule (identical in every role)
   struct Item {
@@ -335,7 +345,10 @@ __global__ void __launch_bounds__(192, 2)
       }
     }
     sync_q(n_taken - 1);  // trailing items without tiles: consume their QFull phases
-  } else {
+  } else if (warp < 4) {
+#if TATN_FWD1_WIDE
+    setmaxnreg_inc<200>();
+#endif
     // ------------------------------------------------------------ softmax + epilogue warpgroup
     const int row = warp * 32 + lane;  // row within the tile == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
