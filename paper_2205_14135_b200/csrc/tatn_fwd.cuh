@@ -47,6 +47,13 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy O rescale (log2 units)
 #define TATN_EMU_PAIRS 1
 #endif
 constexpr int kEmuPairs = TATN_EMU_PAIRS;
+// d = 128 keeps every exp2 on MUFU: there the MMA and MUFU are balanced and the FMA-pipe
+// polynomial measured slower (N = 8K causal fwd 889 -> 912 TFLOP/s without it)
+#ifndef TATN_EMU_PAIRS_D128
+#define TATN_EMU_PAIRS_D128 0
+#endif
+template <int D>
+constexpr int kEmuPairsD = D == 128 ? TATN_EMU_PAIRS_D128 : TATN_EMU_PAIRS;
 
 template <int D, int NQ = 2>
 struct FwdCfg {
@@ -696,7 +703,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
                 pk[k] = ex2_pair16<BF16>(x0, x1);
                 pv = widen_pair16<BF16>(pk[k]);  // l sums exactly the P the MMA consumes
               } else {
-                if (kEmu && (i & 7) < kEmuPairs) {
+                if (kEmu && (i & 7) < kEmuPairsD<D>) {
                   pv = exp2_poly_f2(x);
                 } else {
                   float x0, x1;
@@ -717,7 +724,7 @@ __global__ void __launch_bounds__(fwd_threads<NQ>(), NQ == 2 ? 1 : 2)
             }
           };
           // the polynomial needs finite x: full tiles with m_use <= the true max + threshold
-          if (kEmuPairs > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
+          if (kEmuPairsD<D> > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
           else exp_chunk(std::false_type{});
           tmem_st16(tP + c * 16, pk);
           if (c + 1 < 4) tmem_ld_wait32(nxt);

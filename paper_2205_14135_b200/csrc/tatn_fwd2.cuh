@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(384, 1)
                   pk[k] = ex2_pair16<BF16>(x0, x1);
                   pv = widen_pair16<BF16>(pk[k]);  // l sums exactly the P the MMA consumes
                 } else {
-                  if (kEmu && (i & 7) < kEmuPairs) {
+                  if (kEmu && (i & 7) < kEmuPairsD<D>) {
                     pv = exp2_poly_f2(x);
                   } else {
                     float x0, x1;
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(384, 1)
               }
             };
             // the polynomial needs finite x: full tiles with m_use <= the true max + threshold
-            if (kEmuPairs > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
+            if (kEmuPairsD<D> > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
             else exp_chunk(std::false_type{});
             tmem_st16(tP + c * 16, pk);
             if (c + 1 < 4) tmem_ld_wait32(nxt);
