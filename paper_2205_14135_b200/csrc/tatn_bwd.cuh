@@ -40,6 +40,9 @@
 #ifndef TATN_BWD_SPLIT
 #define TATN_BWD_SPLIT 0  // softmax warpgroups split each Q tile's columns (1) or alternate tiles (0)
 #endif
+#ifndef TATN_BWD_STAGES_D64
+#define TATN_BWD_STAGES_D64 4  // d = 64 Q / dO ring depth
+#endif
 #ifndef TATN_BWD_DS_BUFS
 #define TATN_BWD_DS_BUFS 2  // d = 64 dS^T buffers (3 measured no faster: the softmax is not waiting on them)
 #endif
@@ -64,7 +67,7 @@ struct BwdCfg {
   static constexpr int kQSub = 64 * 128;              // 64 rows x 128B
   static constexpr int kQTile = kSubs * kQSub;        // 64 rows x D x 2B
   // d = 128 with dropout drops to 2 stages to make room for the per-warpgroup row hashes
-  static constexpr int kStages = (D == 128) ? (DROP ? 2 : 3) : 4;
+  static constexpr int kStages = (D == 128) ? (DROP ? 2 : 3) : TATN_BWD_STAGES_D64;
   static constexpr int kDSBytes = 128 * 128;          // 128 keys x 64 q x 2B
   // dS^T shared-memory buffers (tile g uses g % kDSBufs): with 3 at d = 64 the softmax of tile
   // g waits for the dQ^T MMA of tile g - 3, not g - 2 (issued after the front of tile g)
