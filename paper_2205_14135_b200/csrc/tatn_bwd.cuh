@@ -40,6 +40,9 @@
 #ifndef TATN_BWD_SPLIT
 #define TATN_BWD_SPLIT 0  // softmax warpgroups split each Q tile's columns (1) or alternate tiles (0)
 #endif
+#ifndef TATN_BWD_CROSS_ITEM
+#define TATN_BWD_CROSS_ITEM 0  // 1: d = 64 issues the next item's first fronts under this item's last tiles (measured slower)
+#endif
 #ifndef TATN_BWD_STAGES_D64
 #define TATN_BWD_STAGES_D64 4  // d = 64 Q / dO ring depth
 #endif
@@ -522,20 +525,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint64_t dKmn0 = make_sdesc_sw128(sKV, 128 * 128, 1024);       // K^T as MN-major A
     const uint64_t dDS0 = make_sdesc_sw128(sDS, 128 * 128, 1024);        // dS^T as MN-major B
     int g0 = 0;  // Q tiles issued before the current item
-    for (int n = 0;; ++n) {
-      const int w = take_item(n);
-      if (w < 0) break;
+    // d = 64 (double-buffered K/V, separate dQ^T TMEM): the first two fronts of item n + 1 are
+    // issued under the last back-MMAs of item n, as within an item, so the softmax warpgroups
+    // do not wait a full MMA round trip at every item boundary
+    constexpr bool kCross = Cfg::kSepDQ && NKV == 2 && TATN_BWD_CROSS_ITEM;
+    int w_next = take_item(0);
+    int pre = 0;            // fronts of the current item already issued by the previous one
+    bool kv_ready = false;  // KVFull of the current item already consumed
+    for (int n = 0; w_next >= 0; ++n) {
+      const int w = w_next;
       const int cnt = item(w, n).cnt;
       const int kb = n % NKV;
       const uint32_t koff = static_cast<uint32_t>(kb * 2 * Cfg::kKVTile);  // K of buffer kb
       const uint32_t voff = koff + Cfg::kKVTile;
-      mbar_wait(BAR(kBarKVFull + kb), static_cast<uint32_t>((n / NKV) & 1));
-      tc_fence_after();
+      if (!kv_ready) {
+        mbar_wait(BAR(kBarKVFull + kb), static_cast<uint32_t>((n / NKV) & 1));
+        tc_fence_after();
+      }
+      kv_ready = false;
+      bool next_taken = false;
+      int cnt_next = 0, pre_next = 0;
+      const uint32_t koff_next = static_cast<uint32_t>(((n + 1) % NKV) * 2 * Cfg::kKVTile);
       if (lane == 0 && n == 0) TATN_TRACE_AT(1);
 #ifdef TATN_TRACE
       if (lane == 0 && n == 0 && g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 6] = cnt;
 #endif
-      auto front_dp = [&](int g) {  // dP^T = V dO^T  -> X cols [64,128)
+      auto front_dp = [&](int g, uint32_t voff) {  // dP^T = V dO^T  -> X cols [64,128)
         const int s = g % S;
         const int x = g & 1;
         mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>((g / S) & 1));
@@ -557,7 +572,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
       };
-      auto front_s = [&](int g) {  // S^T = K Q^T  -> X cols [0,64)
+      auto front_s = [&](int g, uint32_t koff) {  // S^T = K Q^T  -> X cols [0,64)
         const int s = g % S;
         const int x = g & 1;
         if (elect_one_sync()) {
@@ -583,11 +598,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(BAR(kBarDQEmpty + (g & 1)), static_cast<uint32_t>((g >> 1) & 1));
         tc_fence_after();
       };
-      for (int i = 0; i < cnt && i < 2; ++i) {
+      for (int i = pre; i < cnt && i < 2; ++i) {
         const int g = g0 + i;
-        front_dp(g);
+        front_dp(g, voff);
         if (!Cfg::kSepDQ && g >= 2) wait_dq_drained(g - 2);  // X_x still holds dQ^T(g - 2)
-        front_s(g);
+        front_s(g, koff);
       }
       for (int i = 0; i < cnt; ++i) {
         const int g = g0 + i;
@@ -634,25 +649,63 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // X_x is free once dV/dK have read P^T / dS^T (in-order pipe): start the next front
           // first so S^T(g + 2) reaches the softmax warpgroup one dQ^T earlier
           if (i + 2 < cnt) {
-            front_dp(g + 2);
-            front_s(g + 2);
+            front_dp(g + 2, voff);
+            front_s(g + 2, koff);
           }
           if (g >= 2) wait_dq_drained(g - 2);  // dQ^T buffer x free
           issue_dq();
+          if constexpr (kCross) {
+            if (i + 2 >= cnt) {  // after this item's dQ^T: Final (and the dK/dV epilogue) is not delayed
+              if (i == cnt - 1) {  // the item's last MMA: commit before any front of the next item
+                if (elect_one_sync()) {
+                  mma_commit(BAR(kBarFinal));
+                  mma_commit(BAR(kBarKVFree + kb));
+                }
+                __syncwarp();
+              }
+              if (!next_taken) {  // peek the next item (its ring slot is consumed once, here)
+                w_next = take_item(n + 1);
+                next_taken = true;
+                if (w_next >= 0) cnt_next = item(w_next, n + 1).cnt;
+              }
+              // only if its K/V has already landed: never stall this item's last MMAs on a load
+              if (w_next >= 0 && !kv_ready) {
+                kv_ready = __shfl_sync(0xffffffffu, mbar_try_wait(BAR(kBarKVFull + (n + 1) % NKV),
+                                                                  static_cast<uint32_t>(((n + 1) / NKV) & 1)),
+                                       0);
+                if (kv_ready) tc_fence_after();
+              }
+              // tiles of the next item in order, up to global tile g + 2 (X buffers free in order)
+              auto q_landed = [&](int gt) {  // warp-uniform non-blocking QFull test
+                return __shfl_sync(0xffffffffu,
+                                   mbar_try_wait(BAR(kBarQFull + gt % S), static_cast<uint32_t>((gt / S) & 1)), 0);
+              };
+              while (kv_ready && pre_next < cnt_next && pre_next < 2 && g0 + cnt + pre_next <= g + 2 &&
+                     q_landed(g0 + cnt + pre_next)) {
+                front_dp(g0 + cnt + pre_next, koff_next + Cfg::kKVTile);
+                front_s(g0 + cnt + pre_next, koff_next);
+                ++pre_next;
+              }
+            }
+          }
         } else {
           issue_dq();  // dQ^T lands in X_x cols [0,64): the next front waits for the dQ warpgroup
           if (i + 2 < cnt) {
-            front_dp(g + 2);
+            front_dp(g + 2, voff);
             wait_dq_drained(g);
-            front_s(g + 2);
+            front_s(g + 2, koff);
           }
         }
       }
-      if (elect_one_sync()) {
-        mma_commit(BAR(kBarFinal));
-        mma_commit(BAR(kBarKVFree + kb));
+      if (!(kCross && cnt > 0)) {  // (kCross: committed after the last tile's dQ^T above)
+        if (elect_one_sync()) {
+          mma_commit(BAR(kBarFinal));
+          mma_commit(BAR(kBarKVFree + kb));
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      if (!next_taken) w_next = take_item(n + 1);
+      pre = pre_next;
       g0 += cnt;
     }
   } else if (warp < 8) {
