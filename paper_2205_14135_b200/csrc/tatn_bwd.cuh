@@ -40,6 +40,9 @@
 #ifndef TATN_BWD_SPLIT
 #define TATN_BWD_SPLIT 0  // softmax warpgroups split each Q tile's columns (1) or alternate tiles (0)
 #endif
+#ifndef TATN_BWD_SEP_STAGE
+#define TATN_BWD_SEP_STAGE 1  // d = 64: dK / dV staging in its own shared-memory region
+#endif
 #ifndef TATN_BWD_CROSS_ITEM
 #define TATN_BWD_CROSS_ITEM 0  // 1: d = 64 issues the next item's first fronts under this item's last tiles (measured slower)
 #endif
@@ -93,7 +96,12 @@ struct BwdCfg {
   // d = 128 has no shared memory left for them: block-sparse runs one item per CTA
   static constexpr int kMaskSlots = (D == 64) ? 4 : 1;
   static constexpr int kOffDrop = kOffMask + 512 * kMaskSlots;  // dropout: 64 query-row hashes per softmax warpgroup
-  static constexpr int kSmemBytes = kOffDrop + (DROP ? 1024 : 0);  // dynamic smem is declared __align__(1024)
+  // d = 64: the dK / dV output staging has its own region (d = 128 has no room: it aliases the
+  // dS^T + dQ staging and the next item's first dS^T store waits for the store to read it)
+  static constexpr bool kSepStage = D == 64 && TATN_BWD_SEP_STAGE;
+  static constexpr int kOffStage = ((kOffDrop + (DROP ? 1024 : 0)) + 1023) / 1024 * 1024;
+  static constexpr int kSmemBytes =
+      kSepStage ? kOffStage + 2 * 128 * D * 2 : kOffDrop + (DROP ? 1024 : 0);  // declared __align__(1024)
   static_assert(kSmemBytes <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
   static_assert(2 * 128 * D * 2 <= kOffVec - kOffDS, "dK/dV staging must fit the dS^T + dQ staging region");
   static constexpr uint32_t kTmemX = 0;    // X_x = x*128: S^T [0,64) dP^T [64,128)
@@ -336,7 +344,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t sDO = smem_base + Cfg::kOffDO;
   const uint32_t sDS = smem_base + Cfg::kOffDS;
   const uint32_t sDQ = smem_base + Cfg::kOffDQ;
-  const uint32_t sStage = sDS;  // dK / dV output staging reuses the dS^T + dQ staging region
+  // dK / dV output staging: its own region at d = 64, else the dS^T + dQ staging region
+  const uint32_t sStage = Cfg::kSepStage ? smem_base + Cfg::kOffStage : sDS;
   const uint32_t sVec = smem_base + Cfg::kOffVec;
   const float* vec_gen = reinterpret_cast<const float*>(smem_gen + Cfg::kOffVec);
   const uint32_t bar0 = smem_base + Cfg::kOffBar;
@@ -838,7 +847,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               // the dQ^T MMA of tile g - 2 must have released the dS^T buffer, and in a new
               // item the previous item's dK / dV staging must have been stored
               mbar_wait(BAR(kBarDSEmpty + xs), static_cast<uint32_t>(((g / Cfg::kDSBufs) & 1) ^ 1));
-              if (first) wait_counter_ge(BAR(kBarStageFree), static_cast<uint32_t>(n));
+              if (!Cfg::kSepStage && first) wait_counter_ge(BAR(kBarStageFree), static_cast<uint32_t>(n));
               first = false;
             }
             // dS^T -> smem [key][64 queries], 128B swizzle (B operand of dQ^T, MN-major)
