@@ -185,9 +185,10 @@ class Step:
         self.lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
         self.dq, self.dk, self.dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
         self.ws = A.bwd_workspace(q, k, v, spec)
+        self.fws = A.fwd_workspace(q.device)  # the forward's item counter: zeroed once, reset by the kernel
 
     def fwd(self):
-        self.A.flash_fwd(self.q, self.k, self.v, self.spec, out=self.o, lse=self.lse)
+        self.A.flash_fwd(self.q, self.k, self.v, self.spec, out=self.o, lse=self.lse, workspace=self.fws)
 
     def bwd(self):
         self.A.flash_bwd(self.q, self.k, self.v, self.o, self.do, self.lse, self.spec, self.dq, self.dk, self.dv,

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TATN_B200_ABI_VERSION 3
+#define TATN_B200_ABI_VERSION 4
 
 typedef enum {
   TATN_OK = 0,
@@ -43,13 +43,19 @@ typedef enum {
   TATN_E_WORKSPACE = 6     /* workspace too small                                                */
 } tatn_status;
 
-/* TATN_DTYPE_FP32 is an output type of tatn_merge_partials only. */
+/* Input types. BF16 / FP16: the throughput path (kind::f16 MMAs, fp32 accumulate).
+ * FP32 (ABI v4): the fp32-input check mode — q, k, v, dO are read as fp32 by TMA and
+ * multiplied on the tensor cores as tf32 (kind::tf32, fp32 accumulate; P and dS rounded to
+ * tf32 on chip); every output (o, dq, dk, dv) is fp32 and the backward reads o as fp32.
+ * One CTA per tile, no pipelining: a precision mode for the reference's fp32 oracle shape
+ * (BASELINE configs[0]), not a throughput path. FP32 is also an output type of
+ * tatn_merge_partials. */
 typedef enum { TATN_DTYPE_BF16 = 0, TATN_DTYPE_FP16 = 1, TATN_DTYPE_FP32 = 2 } tatn_dtype;
 
-/* Output precision: O (forward) and dQ/dK/dV (backward) are written either in
- * the 16-bit input dtype or in fp32 (the "fp32 check mode" — no output
- * rounding; the backward then also reads O as fp32). The MMAs always take the
- * 16-bit inputs and accumulate in fp32. */
+/* Output precision of 16-bit inputs: O (forward) and dQ/dK/dV (backward) are written either in
+ * the 16-bit input dtype or in fp32 (no output rounding; the backward then also reads O as
+ * fp32). The MMAs take the 16-bit inputs and accumulate in fp32. Ignored for FP32 inputs
+ * (outputs are fp32). */
 typedef enum { TATN_OUT_INPUT_DTYPE = 0, TATN_OUT_FP32 = 1 } tatn_out_dtype;
 
 /* tatn::MaskKind (attn_config.hpp:12). Causal masks key j > query i;
@@ -66,7 +72,7 @@ typedef struct {
   int32_t B, H;      /* independent (batch, head) slices, each 1..65535           */
   int32_t Nq, Nk;    /* query rows, key rows (Nk <= Nq: key prefix, reference.hpp:43-46) */
   int32_t d;         /* head dimension: 64 or 128                                 */
-  int32_t dtype;     /* tatn_dtype of q, k, v, dO                                 */
+  int32_t dtype;     /* tatn_dtype of q, k, v, dO (BF16, FP16 or FP32)            */
   int32_t out_dtype; /* tatn_out_dtype of o, dq, dk, dv                           */
   /* element strides of the b, h, n dimensions; d is contiguous (stride 1).
    * dO uses o_str; dQ/dK/dV use q_str/k_str/v_str. Strides must be multiples of 8. */
@@ -91,7 +97,8 @@ typedef struct {
   /* Custom mask (MaskSpec::custom_additive, attn_config.hpp:27; ABI v3): bit-packed keep
    * matrix in DEVICE memory, row-major [Nq][custom_words] uint32 per batch element: bit
    * (j & 31) of word (j >> 5) of row i is 1 iff custom(i, j) == 0 (keep), 0 iff -inf.
-   * custom_words >= ceil(Nk/32) and a multiple of 4; custom_bstride = words between batch
+   * custom_words >= 4 * ceil((k_offset + Nk) / 128) (the kernels read word (k_offset + j) / 32,
+   * 16 bytes per 128-key tile) and a multiple of 4; custom_bstride = words between batch
    * elements (0: one mask shared by every slice). NULL unless mask_kind == CUSTOM. */
   const uint32_t* custom_mask;
   int32_t custom_words;
@@ -117,10 +124,17 @@ int tatn_merge_partials(int32_t R, int32_t B, int32_t H, int32_t Nq, int32_t d, 
 /* Host-only descriptor check (no device access); same codes as the compute calls. */
 int tatn_validate(const tatn_attn_desc* desc);
 
+/* Workspace of tatn_fwd (ABI v4): 16 bytes, 16-byte aligned — the persistent kernels' work-item
+ * counter. It must be zero before its first use (e.g. cudaMemset once); every tatn_fwd leaves it
+ * zero again when its kernel completes, so a workspace is reused without re-zeroing. Calls
+ * that may run concurrently (different streams, graphs replayed side by side) need distinct
+ * workspaces; there is no global state in the library. */
+size_t tatn_fwd_workspace_bytes(const tatn_attn_desc* desc);
+
 /* Forward: o = softmax(mask(tau q k^T)) v, lse = natural-log logsumexp per row
  * ([B, H, Nq] contiguous fp32; -inf and o = 0 for fully masked rows). */
 int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, void* o,
-             float* lse, void* stream);
+             float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Workspace for tatn_bwd: fp32 dQ accumulator [B,H,Nq_pad,d] + lse2 and D vectors
  * [B,H,Nq_pad], Nq_pad = Nq rounded up to 128, + 16 bytes (persistent scheduler counter)

@@ -15,7 +15,7 @@ _PKG = Path(__file__).resolve().parent
 # TATN_B200_LIB may point at an alternative in-tree build (tuning experiments); default is the product library
 LIB_PATH = Path(os.environ.get("TATN_B200_LIB", _PKG / "lib" / "libtatn_b200.so"))
 
-ABI_VERSION = 3  # TATN_B200_ABI_VERSION (include/tatn_b200.h)
+ABI_VERSION = 4  # TATN_B200_ABI_VERSION (include/tatn_b200.h)
 
 TATN_OK = 0
 TATN_E_ARG = 1
@@ -27,7 +27,7 @@ TATN_E_WORKSPACE = 6
 
 TATN_DTYPE_BF16 = 0
 TATN_DTYPE_FP16 = 1
-TATN_DTYPE_FP32 = 2  # tatn_merge_partials output only
+TATN_DTYPE_FP32 = 2  # fp32 inputs (tf32 check mode); also a tatn_merge_partials output type
 
 TATN_OUT_INPUT_DTYPE = 0
 TATN_OUT_FP32 = 1
@@ -40,6 +40,7 @@ TATN_MASK_CUSTOM = 3
 # every symbol include/tatn_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED_SYMBOLS = (
     "tatn_validate",
+    "tatn_fwd_workspace_bytes",
     "tatn_fwd",
     "tatn_bwd_workspace_bytes",
     "tatn_bwd",
@@ -109,7 +110,9 @@ def load() -> ctypes.CDLL:
     pd = ctypes.POINTER(TatnAttnDesc)
     lib.tatn_validate.argtypes = [pd]
     lib.tatn_validate.restype = ctypes.c_int
-    lib.tatn_fwd.argtypes = [pd, vp, vp, vp, vp, vp, vp]
+    lib.tatn_fwd_workspace_bytes.argtypes = [pd]
+    lib.tatn_fwd_workspace_bytes.restype = ctypes.c_size_t
+    lib.tatn_fwd.argtypes = [pd, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     lib.tatn_fwd.restype = ctypes.c_int
     lib.tatn_bwd_workspace_bytes.argtypes = [pd]
     lib.tatn_bwd_workspace_bytes.restype = ctypes.c_size_t

@@ -6,7 +6,8 @@ pointers plus the current CUDA stream to ``libtatn_b200.so``. PyTorch provides
 memory and streams only — no attention math happens here.
 
 Tensor layout: ``[B, H, N, d]`` with ``d`` contiguous (any b/h/n strides that
-are multiples of 8 elements), dtype bf16 or fp16, on an sm_100 device.
+are multiples of 8 elements), dtype bf16 or fp16 (the throughput path) or fp32
+(the tf32 check mode: fp32 outputs), on an sm_100 device.
 LSE is ``[B, H, Nq]`` fp32 (natural log).
 """
 from __future__ import annotations
@@ -33,7 +34,14 @@ def _dtype_code(t: torch.Tensor) -> int:
         return _lib.TATN_DTYPE_BF16
     if t.dtype == torch.float16:
         return _lib.TATN_DTYPE_FP16
-    raise TypeError(f"unsupported dtype {t.dtype}: the sm_100a path takes bf16 or fp16")
+    if t.dtype == torch.float32:
+        return _lib.TATN_DTYPE_FP32
+    raise TypeError(f"unsupported dtype {t.dtype}: the sm_100a path takes bf16, fp16 or fp32 (tf32 check mode)")
+
+
+def out_dtype(q: torch.Tensor, spec: "AttnSpec") -> torch.dtype:
+    """dtype of O / dQ / dK / dV: fp32 for fp32 inputs or spec.out_fp32, else the input dtype."""
+    return torch.float32 if (spec.out_fp32 or q.dtype == torch.float32) else q.dtype
 
 
 def _strides(t: torch.Tensor, name: str):
@@ -75,18 +83,38 @@ def pack_custom_mask(keep: torch.Tensor) -> torch.Tensor:
     return torch.where(packed >= 2**31, packed - 2**32, packed).to(torch.int32).contiguous()
 
 
+def _check_vec(t, name, dtype, n, device):
+    if t.dtype != dtype or t.dim() != 1 or t.numel() < n or not t.is_contiguous() or t.device != device:
+        raise ValueError(f"{name} must be a contiguous {dtype} vector of >= {n} elements on {device}, got "
+                         f"{t.dtype} {tuple(t.shape)} on {t.device}")
+
+
 def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttnDesc:
+    """Pack a tatn_attn_desc, checking every shape / dtype / device the ABI cannot see (a
+    descriptor that disagrees with the buffers would let the kernels read or write out of
+    bounds)."""
+    for name, t in (("q", q), ("k", k), ("v", v)) + ((("o", o),) if check_o else ()):
+        if t.dim() != 4:
+            raise ValueError(f"{name} must be [B, H, N, d], got shape {tuple(t.shape)}")
+        if t.device != q.device or t.device.type != "cuda":
+            raise ValueError(f"{name} must be a CUDA tensor on {q.device}, got {t.device}")
     B, H, Nq, d = q.shape
     Nk = k.shape[2]
+    if tuple(k.shape) != (B, H, Nk, d):
+        raise ValueError(f"k shape {tuple(k.shape)} does not match q {tuple(q.shape)} (expected [B, H, Nk, d])")
+    if tuple(v.shape) != tuple(k.shape):
+        raise ValueError(f"v shape {tuple(v.shape)} != k shape {tuple(k.shape)}")
+    if check_o and tuple(o.shape) != tuple(q.shape):
+        raise ValueError(f"o shape {tuple(o.shape)} != q shape {tuple(q.shape)}")
     desc = _lib.TatnAttnDesc()
     desc.B, desc.H, desc.Nq, desc.Nk, desc.d = B, H, Nq, Nk, d
     desc.dtype = _dtype_code(q)
     for t in (k, v):
         if t.dtype != q.dtype:
             raise TypeError("q, k, v must share one dtype")
-    out_dt = torch.float32 if spec.out_fp32 else q.dtype
+    out_dt = out_dtype(q, spec)
     if check_o and o.dtype != out_dt:
-        raise TypeError(f"o must be {out_dt} (out_fp32={spec.out_fp32})")
+        raise TypeError(f"o must be {out_dt} (input {q.dtype}, out_fp32={spec.out_fp32})")
     desc.out_dtype = _lib.TATN_OUT_FP32 if spec.out_fp32 else _lib.TATN_OUT_INPUT_DTYPE
     desc.q_str[:] = _strides(q, "q")
     desc.k_str[:] = _strides(k, "k")
@@ -96,22 +124,32 @@ def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttn
     if spec.mask not in MASK_KINDS:
         raise ValueError(f"unknown mask kind {spec.mask!r}")
     desc.mask_kind = MASK_KINDS[spec.mask]
+    if spec.valid_len is not None:
+        _check_vec(spec.valid_len, "valid_len", torch.int32, B, q.device)
+    elif spec.mask == "key_padding":
+        raise ValueError("mask='key_padding' needs spec.valid_len (int32 [B] on the device)")
     desc.valid_len = spec.valid_len.data_ptr() if spec.valid_len is not None else None
     tr, tc = (Nq + 127) // 128, (Nk + 127) // 128
     if spec.block_grid is not None:
+        g = spec.block_grid
+        if g.dtype != torch.uint8 or g.dim() != 2 or not g.is_contiguous() or g.device != q.device:
+            raise ValueError("block_grid must be a contiguous uint8 [tr, tc] tensor on q's device")
         desc.block_grid = spec.block_grid.data_ptr()
         desc.br = desc.bc = 128
         desc.tr, desc.tc = spec.block_grid.shape
     else:
         desc.block_grid = None
         desc.tr, desc.tc = tr, tc
+    if spec.visited is not None:
+        _check_vec(spec.visited, "visited", torch.int32, (tr * tc + 31) // 32, q.device)
     desc.visited_bitmap = spec.visited.data_ptr() if spec.visited is not None else None
     desc.p_drop = float(spec.p_drop)
     desc.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
     desc.k_offset = int(spec.k_offset)
     if spec.mask == "custom":
         cm = spec.custom
-        if cm is None or cm.dtype != torch.int32 or cm.dim() not in (2, 3) or cm.stride(-1) != 1:
+        if (cm is None or cm.dtype != torch.int32 or cm.dim() not in (2, 3) or not cm.is_contiguous()
+                or cm.device != q.device):
             raise ValueError("mask='custom' needs spec.custom = pack_custom_mask(keep) ([Nq, w] or [B, Nq, w] int32)")
         if cm.shape[-2] != Nq or (cm.dim() == 3 and cm.shape[0] != B):
             raise ValueError(f"custom mask shape {tuple(cm.shape)} does not match B={B}, Nq={Nq}")
@@ -128,19 +166,36 @@ def _check(status: int, what: str):
         raise _lib.TatnError(status, what)
 
 
-def flash_fwd(q, k, v, spec: Optional[AttnSpec] = None, out=None, lse=None, stream=None):
-    """O, LSE = attention forward (kernel K1) on device tensors."""
+FWD_WORKSPACE_BYTES = 16  # tatn_fwd_workspace_bytes() of every valid descriptor
+
+
+def fwd_workspace(device) -> torch.Tensor:
+    """A zeroed forward workspace (the persistent kernels' work-item counter, ABI v4). Every
+    tatn_fwd leaves it zero again, so one workspace serves any number of calls that do not run
+    concurrently (one per stream / per concurrently replayed graph)."""
+    return torch.zeros(FWD_WORKSPACE_BYTES, dtype=torch.uint8, device=device)
+
+
+def flash_fwd(q, k, v, spec: Optional[AttnSpec] = None, out=None, lse=None, stream=None, workspace=None):
+    """O, LSE = attention forward (kernel K1) on device tensors. `workspace`: a zeroed
+    fwd_workspace() reused across sequential calls (default: a fresh one per call)."""
     spec = spec or AttnSpec()
     lib = _lib.load()
     B, H, Nq, d = q.shape
     if out is None:
-        out = torch.empty(q.shape, dtype=torch.float32 if spec.out_fp32 else q.dtype, device=q.device)
+        out = torch.empty(q.shape, dtype=out_dtype(q, spec), device=q.device)
     if lse is None:
         lse = torch.empty((B, H, Nq), dtype=torch.float32, device=q.device)
+    if lse.dtype != torch.float32 or tuple(lse.shape) != (B, H, Nq) or not lse.is_contiguous() or lse.device != q.device:
+        raise ValueError(f"lse must be a contiguous fp32 [B, H, Nq] = {(B, H, Nq)} tensor on {q.device}")
     desc = make_desc(q, k, v, out, spec)
+    if workspace is None:
+        workspace = fwd_workspace(q.device)
+    if workspace.device != q.device or workspace.numel() < FWD_WORKSPACE_BYTES:
+        raise ValueError("workspace must be a >= 16-byte fwd_workspace() on q's device")
     s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
     st = lib.tatn_fwd(ctypes.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                      lse.data_ptr(), s)
+                      lse.data_ptr(), workspace.data_ptr(), workspace.numel(), s)
     _check(st, "tatn_fwd")
     return out, lse
 
@@ -162,11 +217,16 @@ def flash_bwd(q, k, v, o, dO, lse, spec: Optional[AttnSpec] = None, dq=None, dk=
     lib = _lib.load()
     if dO.dtype != q.dtype:
         raise TypeError("dO must have the input dtype")
+    if tuple(dO.shape) != tuple(q.shape) or tuple(o.shape) != tuple(q.shape):
+        raise ValueError(f"o {tuple(o.shape)} and dO {tuple(dO.shape)} must have q's shape {tuple(q.shape)}")
+    B, H, Nq, _ = q.shape
+    if lse.dtype != torch.float32 or tuple(lse.shape) != (B, H, Nq) or not lse.is_contiguous() or lse.device != q.device:
+        raise ValueError(f"lse must be a contiguous fp32 [B, H, Nq] = {(B, H, Nq)} tensor on {q.device}")
     if dO.stride() != o.stride():
         fixed = torch.empty_strided(o.shape, o.stride(), dtype=dO.dtype, device=dO.device)
         fixed.copy_(dO)
         dO = fixed
-    gdt = torch.float32 if spec.out_fp32 else q.dtype
+    gdt = out_dtype(q, spec)
     mk = lambda t: torch.empty_strided(t.shape, t.stride(), dtype=gdt, device=t.device)
     dq = mk(q) if dq is None else dq
     dk = mk(k) if dk is None else dk
@@ -179,6 +239,8 @@ def flash_bwd(q, k, v, o, dO, lse, spec: Optional[AttnSpec] = None, dq=None, dk=
     desc = make_desc(q, k, v, o, spec)
     if workspace is None:
         workspace = bwd_workspace(q, k, v, spec)
+    if workspace.device != q.device:
+        raise ValueError("workspace must be on q's device")
     s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
     st = lib.tatn_bwd(ctypes.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                       dO.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),

@@ -37,14 +37,8 @@
 #include "tatn_params.h"
 #include "tatn_launch.h"
 
-#ifndef TATN_BWD_SPLIT
-#define TATN_BWD_SPLIT 0  // softmax warpgroups split each Q tile's columns (1) or alternate tiles (0)
-#endif
 #ifndef TATN_BWD_SEP_STAGE
 #define TATN_BWD_SEP_STAGE 1  // d = 64: dK / dV staging in its own shared-memory region
-#endif
-#ifndef TATN_BWD_CROSS_ITEM
-#define TATN_BWD_CROSS_ITEM 0  // 1: d = 64 issues the next item's first fronts under this item's last tiles (measured slower)
 #endif
 #ifndef TATN_BWD_STAGES_D64
 #define TATN_BWD_STAGES_D64 4  // d = 64 Q / dO ring depth
@@ -59,10 +53,6 @@
 namespace tatn_dev {
 
 constexpr int kBwdThreads = 448;
-#ifndef TATN_BWD_EMU_PAIRS
-#define TATN_BWD_EMU_PAIRS 0  // exp2 pairs per 8 computed by the FMA-pipe polynomial (unmasked tiles)
-#endif
-constexpr int kBwdEmuPairs = TATN_BWD_EMU_PAIRS;
 constexpr int kBwdQT = 64;    // query rows per Q tile
 constexpr int kBwdKT = 128;   // keys per CTA
 
@@ -118,7 +108,6 @@ struct BwdCfg {
   // d = 64: dQ^T by an M = 64 MMA. Its rows live in TMEM lanes 0-15 of each 32-lane
   // quadrant (row = 16 * quadrant + lane).
   static constexpr bool kDQ64 = D == 64;
-  static constexpr bool kSplit = TATN_BWD_SPLIT != 0;
 };
 
 struct BwdSched {
@@ -179,8 +168,9 @@ __device__ __forceinline__ BwdSched make_bwd_sched(const BwdParams& p, int b, in
 // One 8-element chunk per thread; grid (row blocks, H, B) so no thread divides 64-bit indices
 // (the divisions cost as much issue time as the bytes these HBM-bound kernels move). Rows are
 // padded to a multiple of 128.
-template <int D, bool BF16, bool O_F32>
-__global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_, const uint16_t* __restrict__ dO,
+// DO_F32: dO (and O) are fp32 — the fp32-input check mode (tatn_tf32.cuh)
+template <int D, bool BF16, bool O_F32, bool DO_F32 = false>
+__global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_, const void* __restrict__ dO_,
                                                     const float* __restrict__ lse, int64_t ob, int64_t oh, int64_t on,
                                                     int B, int H, int Nq, int Nq_pad, float* __restrict__ lse2,
                                                     float* __restrict__ delta, float* __restrict__ dq_acc,
@@ -200,9 +190,24 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_,
   if (qi < Nq_pad) {
     if (qi < Nq) {
       const size_t off = static_cast<size_t>(b) * ob + static_cast<size_t>(h) * oh + static_cast<size_t>(qi) * on + c * 8;
-      const uint4 dv = *reinterpret_cast<const uint4*>(dO + off);
-      const uint32_t* dw = reinterpret_cast<const uint32_t*>(&dv);
-      float of[8];
+      float of[8], df[8];
+      if constexpr (DO_F32) {
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(dO_) + off);
+        const float4 a0 = src[0], a1 = src[1];
+        df[0] = a0.x; df[1] = a0.y; df[2] = a0.z; df[3] = a0.w;
+        df[4] = a1.x; df[5] = a1.y; df[6] = a1.z; df[7] = a1.w;
+      } else {
+        const uint4 dv = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dO_) + off);
+        const uint32_t* dw = reinterpret_cast<const uint32_t*>(&dv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float2 bb;
+          if constexpr (BF16) bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dw[k]));
+          else bb = __half22float2(*reinterpret_cast<const __half2*>(&dw[k]));
+          df[2 * k] = bb.x;
+          df[2 * k + 1] = bb.y;
+        }
+      }
       if constexpr (O_F32) {
         const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(o_) + off);
         const float4 a0 = src[0], a1 = src[1];
@@ -221,13 +226,7 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_,
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float2 bb;
-        if constexpr (BF16) bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dw[k]));
-        else bb = __half22float2(*reinterpret_cast<const __half2*>(&dw[k]));
-        part = fmaf(of[2 * k], bb.x, part);
-        part = fmaf(of[2 * k + 1], bb.y, part);
-      }
+      for (int k = 0; k < 8; ++k) part = fmaf(of[k], df[k], part);
     }
     float4* dst = reinterpret_cast<float4*>(dq_acc + row * D + c * 8);
     dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -394,7 +393,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (i != kBarStageFree) mbar_init(BAR(i), 1);
     *reinterpret_cast<volatile uint64_t*>(smem_gen + Cfg::kOffBar + 8 * kBarStageFree) = 0;
     for (int x = 0; x < 2; ++x) {
-      mbar_init(BAR(kBarPFull + x), Cfg::kSplit ? 256 : 128);
+      mbar_init(BAR(kBarPFull + x), 128);
       mbar_init(BAR(kBarDQEmpty + x), 128);
     }
     mbar_init(BAR(kBarAccFree), 128);
@@ -534,27 +533,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint64_t dKmn0 = make_sdesc_sw128(sKV, 128 * 128, 1024);       // K^T as MN-major A
     const uint64_t dDS0 = make_sdesc_sw128(sDS, 128 * 128, 1024);        // dS^T as MN-major B
     int g0 = 0;  // Q tiles issued before the current item
-    // d = 64 (double-buffered K/V, separate dQ^T TMEM): the first two fronts of item n + 1 are
-    // issued under the last back-MMAs of item n, as within an item, so the softmax warpgroups
-    // do not wait a full MMA round trip at every item boundary
-    constexpr bool kCross = Cfg::kSepDQ && NKV == 2 && TATN_BWD_CROSS_ITEM;
     int w_next = take_item(0);
-    int pre = 0;            // fronts of the current item already issued by the previous one
-    bool kv_ready = false;  // KVFull of the current item already consumed
     for (int n = 0; w_next >= 0; ++n) {
       const int w = w_next;
       const int cnt = item(w, n).cnt;
       const int kb = n % NKV;
       const uint32_t koff = static_cast<uint32_t>(kb * 2 * Cfg::kKVTile);  // K of buffer kb
       const uint32_t voff = koff + Cfg::kKVTile;
-      if (!kv_ready) {
-        mbar_wait(BAR(kBarKVFull + kb), static_cast<uint32_t>((n / NKV) & 1));
-        tc_fence_after();
-      }
-      kv_ready = false;
-      bool next_taken = false;
-      int cnt_next = 0, pre_next = 0;
-      const uint32_t koff_next = static_cast<uint32_t>(((n + 1) % NKV) * 2 * Cfg::kKVTile);
+      mbar_wait(BAR(kBarKVFull + kb), static_cast<uint32_t>((n / NKV) & 1));
+      tc_fence_after();
       if (lane == 0 && n == 0) TATN_TRACE_AT(1);
 #ifdef TATN_TRACE
       if (lane == 0 && n == 0 && g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 6] = cnt;
@@ -569,14 +556,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t offa = voff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
             const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
-#ifdef TATN_EXP_TS_FRONT  // timing experiment only: A operand from (garbage) TMEM
-            mma_ts(tmem_base + Cfg::kTmemX + x * 128 + 64, tmem_base + Cfg::kTmemDQ + kk * 8,
-                   dDOk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
-            (void)offa;
-#else
             mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, dKV0 + (offa >> 4),
                    dDOk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
-#endif
           }
         }
         __syncwarp();
@@ -589,14 +570,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t offa = koff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
             const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
-#ifdef TATN_EXP_TS_FRONT
-            mma_ts(tmem_base + Cfg::kTmemX + x * 128, tmem_base + Cfg::kTmemDQ + 32 + kk * 8,
-                   dQk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s, kk > 0 ? 1u : 0u);
-            (void)offa;
-#else
             mma_ss(tmem_base + Cfg::kTmemX + x * 128, dKV0 + (offa >> 4), dQk0 + ((s * Cfg::kQTile + offb) >> 4),
                    idesc_s, kk > 0 ? 1u : 0u);
-#endif
           }
           mma_commit(BAR(kBarSFull + x));
         }
@@ -607,7 +582,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(BAR(kBarDQEmpty + (g & 1)), static_cast<uint32_t>((g >> 1) & 1));
         tc_fence_after();
       };
-      for (int i = pre; i < cnt && i < 2; ++i) {
+      for (int i = 0; i < cnt && i < 2; ++i) {
         const int g = g0 + i;
         front_dp(g, voff);
         if (!Cfg::kSepDQ && g >= 2) wait_dq_drained(g - 2);  // X_x still holds dQ^T(g - 2)
@@ -663,40 +638,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           if (g >= 2) wait_dq_drained(g - 2);  // dQ^T buffer x free
           issue_dq();
-          if constexpr (kCross) {
-            if (i + 2 >= cnt) {  // after this item's dQ^T: Final (and the dK/dV epilogue) is not delayed
-              if (i == cnt - 1) {  // the item's last MMA: commit before any front of the next item
-                if (elect_one_sync()) {
-                  mma_commit(BAR(kBarFinal));
-                  mma_commit(BAR(kBarKVFree + kb));
-                }
-                __syncwarp();
-              }
-              if (!next_taken) {  // peek the next item (its ring slot is consumed once, here)
-                w_next = take_item(n + 1);
-                next_taken = true;
-                if (w_next >= 0) cnt_next = item(w_next, n + 1).cnt;
-              }
-              // only if its K/V has already landed: never stall this item's last MMAs on a load
-              if (w_next >= 0 && !kv_ready) {
-                kv_ready = __shfl_sync(0xffffffffu, mbar_try_wait(BAR(kBarKVFull + (n + 1) % NKV),
-                                                                  static_cast<uint32_t>(((n + 1) / NKV) & 1)),
-                                       0);
-                if (kv_ready) tc_fence_after();
-              }
-              // tiles of the next item in order, up to global tile g + 2 (X buffers free in order)
-              auto q_landed = [&](int gt) {  // warp-uniform non-blocking QFull test
-                return __shfl_sync(0xffffffffu,
-                                   mbar_try_wait(BAR(kBarQFull + gt % S), static_cast<uint32_t>((gt / S) & 1)), 0);
-              };
-              while (kv_ready && pre_next < cnt_next && pre_next < 2 && g0 + cnt + pre_next <= g + 2 &&
-                     q_landed(g0 + cnt + pre_next)) {
-                front_dp(g0 + cnt + pre_next, koff_next + Cfg::kKVTile);
-                front_s(g0 + cnt + pre_next, koff_next);
-                ++pre_next;
-              }
-            }
-          }
         } else {
           issue_dq();  // dQ^T lands in X_x cols [0,64): the next front waits for the dQ warpgroup
           if (i + 2 < cnt) {
@@ -706,23 +647,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
       }
-      if (!(kCross && cnt > 0)) {  // (kCross: committed after the last tile's dQ^T above)
-        if (elect_one_sync()) {
-          mma_commit(BAR(kBarFinal));
-          mma_commit(BAR(kBarKVFree + kb));
-        }
-        __syncwarp();
+      if (elect_one_sync()) {
+        mma_commit(BAR(kBarFinal));
+        mma_commit(BAR(kBarKVFree + kb));
       }
-      if (!next_taken) w_next = take_item(n + 1);
-      pre = pre_next;
+      __syncwarp();
+      w_next = take_item(n + 1);
       g0 += cnt;
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax warpgroups
-    // kSplit: both warpgroups work on every Q tile, warpgroup sg on query columns
-    // [32 sg, 32 sg + 32) (halves the per-tile latency of the softmax step); otherwise
-    // warpgroup sg takes the Q tiles of parity sg (ping-pong over the two X buffers).
-    constexpr bool kSplit = Cfg::kSplit;
+    // warpgroup sg takes the Q tiles of parity sg (ping-pong over the two X buffers)
     const int sg = warp >> 2;
     const int r = (warp & 3) * 32 + lane;   // key row within tile == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -740,9 +675,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       bool first = true;  // first dS^T store of this warpgroup in this item
       int g = g0;
       for (int i = sc.next(sc.i_begin); i < sc.i_end; i = sc.next(i + 1), ++g) {
-        if (!kSplit && (g & 1) != sg) continue;
+        if ((g & 1) != sg) continue;
         const int s = g % S;
-        const int x = g & 1;  // X buffer (== sg without kSplit)
+        const int x = g & 1;  // X buffer (== sg)
         const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + x * 128;
         if (p.visited != nullptr && r == 0) {
           const long long bit = static_cast<long long>(i >> 1) * p.tc + it.j;
@@ -777,11 +712,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             cbits = *reinterpret_cast<const uint2*>(
                 p.custom_t + (static_cast<size_t>(p.custom_t_b ? it.b : 0) * p.Nk + kj) * p.custom_t_words + i * 2);
         }
-        constexpr int kH0 = 0, kH1 = kSplit ? 1 : 2;  // halves (32 query columns) per warpgroup
-        const int hbase = kSplit ? sg : 0;
         uint32_t sr[32], dp[32];
-        tmem_ld32_async(tX + 32 * hbase, sr);
-        tmem_ld32_async(tX + 64 + 32 * hbase, dp);
+        tmem_ld32_async(tX, sr);
+        tmem_ld32_async(tX + 64, dp);
         tmem_ld_wait32(sr);
         tmem_ld_wait32(dp);
         if (D == 64 && r == 0) TATN_EV(g, 6);
@@ -790,8 +723,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         auto body = [&](auto masked_t) {
           constexpr bool kMasked = decltype(masked_t)::value;
 #pragma unroll
-          for (int hh = kH0; hh < kH1; ++hh) {
-            const int half = hbase + hh;
+          for (int half = 0; half < 2; ++half) {
             // queries [32*half, 32*half + 32); half 1 is loaded while half 0's results are stored
             uint32_t pk[16], dk[16];
 #pragma unroll
@@ -806,13 +738,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 const uint64_t xv = f2_fma(f2_pack(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sl2x2,
                                            e ? l4.y : l4.x);
                 float p0, p1;
-                if (!kMasked && !DROP && kBwdEmuPairs > 0 && (k & 7) < kBwdEmuPairs) {
-                  f2_unpack(exp2_poly_f2(xv), p0, p1);  // FMA pipe: relieves MUFU (x <= 0 here)
-                } else {
-                  f2_unpack(xv, p0, p1);
-                  p0 = ex2_approx(p0);
-                  p1 = ex2_approx(p1);
-                }
+                f2_unpack(xv, p0, p1);
+                p0 = ex2_approx(p0);
+                p1 = ex2_approx(p1);
                 if constexpr (kMasked) {
                   const uint32_t cwv = (c < 32) ? cbits.x : cbits.y;
                   p0 = (c < c_lo || ((cwv >> (c & 31)) & 1u) == 0u) ? 0.f : p0;
@@ -837,13 +765,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
               }
             }
-            if (!kSplit && hh == 0) {
+            if (half == 0) {
               tmem_ld32_async(tX + 32, sr);
               tmem_ld32_async(tX + 96, dp);
             }
             tmem_st16(tX + half * 16, pk);       // P^T   -> X cols [0,32)
             tmem_st16(tX + 64 + half * 16, dk);  // dS^T  -> X cols [64,96)
-            if (hh == 0) {
+            if (half == 0) {
               // the dQ^T MMA of tile g - 2 must have released the dS^T buffer, and in a new
               // item the previous item's dK / dV staging must have been stored
               mbar_wait(BAR(kBarDSEmpty + xs), static_cast<uint32_t>(((g / Cfg::kDSBufs) & 1) ^ 1));
@@ -856,7 +784,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               const int chunk = half * 4 + cc;
               st_shared_v4(drow + ((chunk ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
             }
-            if (!kSplit && hh == 0) {
+            if (half == 0) {
               tmem_ld_wait32(sr);
               tmem_ld_wait32(dp);
             }
@@ -907,9 +835,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         mbar_arrive(BAR(kBarDQEmpty + x));
         // staging buffer free once the previous bulk reduce has read it
-#ifdef TATN_EXP_NO_DQ
-        if (true) continue;  // timing experiment only: skip the dQ staging and reduction
-#endif
         if constexpr (Cfg::kDQRed) {
         // fire-and-forget fp32 reductions straight from registers into the L2-resident
         // accumulator: lanes hold consecutive head-dim columns, so each instruction is one
@@ -1040,9 +965,11 @@ inline void set_dropout(const tatn_attn_desc& d, uint64_t* seed, uint64_t* thres
 }
 cudaEvent_t profile_begin(int which, cudaStream_t s);
 int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm);
+constexpr int kMaxDevices = 64;
 int sm_count();
+cudaError_t ensure_smem_attr(const void* kern, int bytes);
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
-                     int box_rows);
+                     int box_rows, bool mn_major = false);
 }
 
 template <int D, bool BF16, bool OUT_F32, bool DROP>
@@ -1071,7 +998,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   {
     const dim3 blocks(static_cast<unsigned>((Nq_pad + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
     cudaError_t e = tatn_host::launch(tatn_dev::tatn_bwd_pre<D, BF16, OUT_F32>, blocks, dim3(256), 0, stream, o,
-                                      static_cast<const uint16_t*>(dO), lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
+                                      dO, lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B,
                                       d.H, d.Nq, Nq_pad, lse2, delta, dq_acc, item_counter);
     if (e != cudaSuccess) return e;
   }
@@ -1120,11 +1047,9 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.v_sn = d.v_str[2];
   tatn_host::set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
   auto kern = tatn_dev::tatn_bwd_kernel<D, BF16, OUT_F32, DROP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+  {
+    cudaError_t e = tatn_host::ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   // persistent, one CTA per SM looping over items (d = 128 block-sparse: one CTA per item, the grid
   // column read once into a shared-memory bitmask)

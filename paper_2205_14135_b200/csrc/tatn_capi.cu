@@ -22,6 +22,7 @@
 #include "tatn_fwd.cuh"
 #include "tatn_fwd1.cuh"
 #include "tatn_fwd2.cuh"
+#include "tatn_tf32.cuh"
 
 namespace tatn_host {
 int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int ctas_per_sm = 1);
@@ -30,26 +31,12 @@ int sm_count();
 using tatn_host::set_dropout;
 using tatn_host::schedule_group;
 
-// Self-resetting item counters of the persistent d = 64 forward ({next, finished CTAs} per slot),
-// handed out round-robin per launch so concurrent launches on different streams do not share one.
-__device__ int g_tatn_fwd_ctr[2 * 64];
-
 namespace {
 
 thread_local int g_last_launches = 0;
-
-int* fwd_counter() {
-  static std::atomic<unsigned> rr{0};
-  static int* base[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (base[dev] == nullptr) {
-    void* p = nullptr;
-    if (cudaGetSymbolAddress(&p, g_tatn_fwd_ctr) != cudaSuccess) return nullptr;
-    base[dev] = static_cast<int*>(p);
-  }
-  return base[dev] + 2 * (rr.fetch_add(1) % 64);
-}
+// forward workspace: the persistent kernels' self-resetting item counter {next item, finished
+// CTAs}; zero before first use, left zero by every completed launch
+constexpr size_t kFwdWorkspaceBytes = 16;
 
 // ---- optional event timing of the main kernels (tatn_profile_*)
 struct Profiler {
@@ -128,7 +115,9 @@ int validate(const tatn_attn_desc* d) {
   if (d->B > 65535 || d->H > 65535) return TATN_E_SHAPE;  // K2 / K4 grid (rows, H, B)
   if (d->Nk > d->Nq) return TATN_E_SHAPE;  // more keys than n (reference.cpp:25-26)
   if (d->d != 64 && d->d != 128) return TATN_E_UNSUPPORTED;
-  if (d->dtype != TATN_DTYPE_BF16 && d->dtype != TATN_DTYPE_FP16) return TATN_E_UNSUPPORTED;
+  // bf16 / fp16 inputs (the throughput path) or fp32 inputs (the tf32 check mode, tatn_tf32.cuh)
+  if (d->dtype != TATN_DTYPE_BF16 && d->dtype != TATN_DTYPE_FP16 && d->dtype != TATN_DTYPE_FP32)
+    return TATN_E_UNSUPPORTED;
   if (d->out_dtype != TATN_OUT_INPUT_DTYPE && d->out_dtype != TATN_OUT_FP32) return TATN_E_UNSUPPORTED;
   if (!(d->tau > 0.f) || !std::isfinite(d->tau)) return TATN_E_ARG;  // attn_config.cpp:52
   if (!(d->p_drop >= 0.0 && d->p_drop < 1.0)) return TATN_E_ARG;      // attn_config.cpp:54
@@ -139,7 +128,10 @@ int validate(const tatn_attn_desc* d) {
   if (d->mask_kind == TATN_MASK_CUSTOM) {
     // custom mask must cover Nq x Nk (attn_config.cpp:50-52: "custom mask must be n x n")
     if (d->custom_mask == nullptr) return TATN_E_ARG;
-    if (d->custom_words < (d->Nk + 31) / 32 || (d->custom_words % 4) != 0) return TATN_E_MASK;
+    // the kernels read word (k_offset + j) / 32 of each row, 16 bytes per 128-key tile
+    if (d->k_offset < 0) return TATN_E_SHAPE;
+    const int64_t need_words = 4 * ((static_cast<int64_t>(d->k_offset) + d->Nk + 127) / 128);
+    if (d->custom_words < need_words || (d->custom_words % 4) != 0) return TATN_E_MASK;
     if (d->custom_bstride != 0 && d->custom_bstride < static_cast<int64_t>(d->Nq) * d->custom_words) return TATN_E_MASK;
     if ((reinterpret_cast<uintptr_t>(d->custom_mask) & 15u) != 0) return TATN_E_ARG;  // 16-byte row loads
   }
@@ -166,37 +158,19 @@ CUtensorMapDataType tma_dtype(int dtype) {
   return dtype == TATN_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
 }
 
-#ifndef TATN_FWD_NQ_D64
-#define TATN_FWD_NQ_D64 1  // d = 64: one Q tile per CTA, two CTAs per SM
-#endif
-#ifndef TATN_FWD_PERSISTENT
-#define TATN_FWD_PERSISTENT 1  // d = 64: persistent kernel (tatn_fwd1.cuh)
-#endif
-#ifndef TATN_FWD_D64_PAIRS
-#define TATN_FWD_D64_PAIRS 0  // experiment: d = 64 on the Q-tile-pair kernel (tatn_fwd2.cuh)
-#endif
-#ifndef TATN_FWD2_PERSISTENT
-#define TATN_FWD2_PERSISTENT 1  // d = 128: persistent kernel (tatn_fwd2.cuh)
-#endif
 template <bool BF16, bool OUT_F32, bool DROP>
 cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
-                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
+                        const tatn_dev::FwdParams& p, int* ctr, cudaStream_t stream) {
   using Cfg = tatn_dev::Fwd1Cfg;
   auto kern = tatn_dev::tatn_fwd1_kernel<BF16, OUT_F32, DROP>;
-  static bool attr_set = false;  // benign race: idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = tatn_host::ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
   tatn_dev::FwdParams pp = p;
   pp.n_pairs = (p.Nq + 127) / 128;  // Q tiles per (b, h)
   pp.n_items = p.B * p.H * pp.n_pairs;
   // persistent + dynamic claims: one head group (global longest-first order) unless the heads'
   // K/V would not stay L2-resident, so no group boundary brings heavy items back into the tail
   pp.group = schedule_group(p.B * p.H, 1, static_cast<double>(p.Nk) * 64 * 4.0, 2);
-  int* ctr = fwd_counter();
-  if (ctr == nullptr) return cudaErrorInvalidValue;
   // persistent: two CTAs per SM
   const int grid = std::min(pp.n_items, 2 * tatn_host::sm_count());
   return tatn_host::launch(kern, dim3(grid), dim3(tatn_dev::kFwd1Threads), Cfg::kSmemBytes, stream, q, k, v, o, pp,
@@ -205,49 +179,108 @@ cudaError_t launch_fwd1(const CUtensorMap& q, const CUtensorMap& k, const CUtens
 
 template <int D, bool BF16, bool OUT_F32, bool DROP>
 cudaError_t launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                        const tatn_dev::FwdParams& p, cudaStream_t stream) {
+                        const tatn_dev::FwdParams& p, int* ctr, cudaStream_t stream) {
   using Cfg = tatn_dev::Fwd2Cfg<D>;
   auto kern = tatn_dev::tatn_fwd2_kernel<D, BF16, OUT_F32, DROP>;
-  static bool attr_set = false;  // benign race: idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = tatn_host::ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
   tatn_dev::FwdParams pp = p;
   pp.n_pairs = (p.Nq + 255) / 256;  // Q-tile pairs per (b, h)
   pp.n_items = p.B * p.H * pp.n_pairs;
   pp.group = schedule_group(p.B * p.H, 1, static_cast<double>(p.Nk) * D * 4.0, 1);
-  int* ctr = fwd_counter();
-  if (ctr == nullptr) return cudaErrorInvalidValue;
   const int grid = std::min(pp.n_items, tatn_host::sm_count());  // persistent, one CTA per SM
   return tatn_host::launch(kern, dim3(grid), dim3(384), Cfg::kSmemBytes, stream, q, k, v, pp, ctr);
 }
 
-template <int D, bool BF16, bool OUT_F32, bool DROP, int NQ = (D == 64 ? TATN_FWD_NQ_D64 : 2)>
+// d = 64: tatn_fwd1 (persistent, one Q tile per item, 2 CTAs/SM); d = 128: tatn_fwd2 (persistent,
+// Q-tile pairs, 1 CTA/SM). Both claim items from the caller's workspace counter.
+template <int D, bool BF16, bool OUT_F32, bool DROP>
 cudaError_t launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
-                       const tatn_dev::FwdParams& p, cudaStream_t stream) {
-  if constexpr (D == 64 && TATN_FWD_D64_PAIRS) {
-    return launch_fwd2<64, BF16, OUT_F32, DROP>(q, k, v, p, stream);
-  } else if constexpr (D == 64 && TATN_FWD_PERSISTENT) {
-    return launch_fwd1<BF16, OUT_F32, DROP>(q, k, v, o, p, stream);
-  } else if constexpr (D == 128 && TATN_FWD2_PERSISTENT) {
-    return launch_fwd2<128, BF16, OUT_F32, DROP>(q, k, v, p, stream);
-  } else {
-    using Cfg = tatn_dev::FwdCfg<D, NQ>;
-    auto kern = tatn_dev::tatn_fwd_kernel<D, BF16, OUT_F32, NQ, DROP>;
-    static bool attr_set = false;  // benign race: idempotent
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-      if (e != cudaSuccess) return e;
-      attr_set = true;
-    }
-    tatn_dev::FwdParams pp = p;
-    pp.n_pairs = (p.Nq + 128 * NQ - 1) / (128 * NQ);  // Q-tile groups (of NQ tiles) per head
-    pp.group = schedule_group(p.B * p.H, pp.n_pairs, static_cast<double>(p.Nk) * D * 4.0, NQ == 2 ? 1 : 2);
-    dim3 grid(static_cast<unsigned>(p.B * p.H * pp.n_pairs));
-    return tatn_host::launch(kern, grid, dim3(tatn_dev::fwd_threads<NQ>()), Cfg::kSmemBytes, stream, q, k, v, o, pp);
-  }
+                       const tatn_dev::FwdParams& p, int* ctr, cudaStream_t stream) {
+  if constexpr (D == 64) return launch_fwd1<BF16, OUT_F32, DROP>(q, k, v, o, p, ctr, stream);
+  else return launch_fwd2<128, BF16, OUT_F32, DROP>(q, k, v, p, ctr, stream);
+}
+
+// fp32 inputs: the tf32 check-mode forward, one CTA per (Q tile, h, b)
+template <int D, bool DROP>
+cudaError_t launch_fwd_tf32(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                            const tatn_dev::FwdParams& p, cudaStream_t stream) {
+  using Cfg = tatn_dev::Tf32FwdCfg<D>;
+  auto kern = tatn_dev::tatn_fwd_tf32_kernel<D, DROP>;
+  cudaError_t e = tatn_host::ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  const dim3 grid(static_cast<unsigned>((p.Nq + 127) / 128), p.H, p.B);
+  return tatn_host::launch(kern, grid, dim3(tatn_dev::kTf32Threads), Cfg::kSmemBytes, stream, q, k, v, p);
+}
+
+// fp32 inputs: K2 (fp32 O, dO) -> the tf32 check-mode backward, one CTA per (key tile, h, b) -> K4
+template <int D, bool DROP>
+cudaError_t launch_bwd_tf32(const tatn_attn_desc& d, const void* q, const void* k, const void* v, const void* o,
+                            const void* dO, const float* lse, void* dq, void* dk, void* dv, void* ws,
+                            cudaStream_t stream, int* launches) {
+  using Cfg = tatn_dev::Tf32BwdCfg<D>;
+  const int Nq_pad = (d.Nq + 127) / 128 * 128;
+  const size_t rows = static_cast<size_t>(d.B) * d.H * Nq_pad;
+  float* dq_acc = static_cast<float*>(ws);
+  float* lse2 = dq_acc + rows * D;
+  float* delta = lse2 + rows;
+  int* item_counter = reinterpret_cast<int*>(delta + rows);
+  const dim3 rblocks(static_cast<unsigned>((Nq_pad + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
+  cudaError_t e = tatn_host::launch(tatn_dev::tatn_bwd_pre<D, false, true, true>, rblocks, dim3(256), 0, stream, o, dO,
+                                    lse, d.o_str[0], d.o_str[1], d.o_str[2], d.B, d.H, d.Nq, Nq_pad, lse2, delta,
+                                    dq_acc, item_counter);
+  if (e != cudaSuccess) return e;
+  CUtensorMap mq, mk, mkmn, mdo;
+  if (!tatn_host::make_map_4d_ext(&mq, TATN_DTYPE_FP32, q, D, d.Nq, d.H, d.B, d.q_str, Cfg::QT) ||
+      !tatn_host::make_map_4d_ext(&mk, TATN_DTYPE_FP32, k, D, d.Nk, d.H, d.B, d.k_str, 128) ||
+      !tatn_host::make_map_4d_ext(&mkmn, TATN_DTYPE_FP32, k, D, d.Nk, d.H, d.B, d.k_str, 128, /*mn_major=*/true) ||
+      !tatn_host::make_map_4d_ext(&mdo, TATN_DTYPE_FP32, dO, D, d.Nq, d.H, d.B, d.o_str, Cfg::QT))
+    return cudaErrorInvalidValue;
+  tatn_dev::BwdParams p{};
+  p.B = d.B;
+  p.H = d.H;
+  p.Nq = d.Nq;
+  p.Nk = d.Nk;
+  p.scale_log2 = d.tau * 1.4426950408889634f;
+  p.tau = d.tau;
+  p.mask_kind = d.mask_kind;
+  p.valid_len = d.valid_len;
+  p.grid = d.block_grid;
+  p.tr = (d.Nq + 127) / 128;
+  p.tc = (d.Nk + 127) / 128;
+  p.visited = d.visited_bitmap;
+  p.lse = lse;
+  p.delta = delta;
+  p.dq_acc = dq_acc;
+  p.dk_f32 = static_cast<float*>(dk);
+  p.dv_f32 = static_cast<float*>(dv);
+  p.k_sb = d.k_str[0];
+  p.k_sh = d.k_str[1];
+  p.k_sn = d.k_str[2];
+  p.v_sb = d.v_str[0];
+  p.v_sh = d.v_str[1];
+  p.v_sn = d.v_str[2];
+  p.k_off = d.k_offset;
+  p.custom = d.mask_kind == TATN_MASK_CUSTOM ? d.custom_mask : nullptr;
+  p.custom_words = d.custom_words;
+  p.custom_bstride = d.custom_bstride;
+  set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
+  auto kern = tatn_dev::tatn_bwd_tf32_kernel<D, DROP>;
+  e = tatn_host::ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t prof_stop = prof_begin(1, stream);
+  e = tatn_host::launch(kern, dim3(static_cast<unsigned>(p.tc), d.H, d.B), dim3(tatn_dev::kTf32Threads),
+                        Cfg::kSmemBytes, stream, mq, mk, mkmn, mdo, static_cast<const float*>(v), p,
+                        static_cast<const float*>(lse2), Nq_pad);
+  if (prof_stop) cudaEventRecord(prof_stop, stream);
+  if (e != cudaSuccess) return e;
+  const dim3 qblocks(static_cast<unsigned>((d.Nq + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
+  e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, false, true>, qblocks, dim3(256), 0, stream,
+                        static_cast<const float*>(dq_acc), dq, d.q_str[0], d.q_str[1], d.q_str[2], d.B, d.H, d.Nq,
+                        Nq_pad);
+  if (e != cudaSuccess) return e;
+  *launches = 3;
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -263,18 +296,43 @@ int schedule_group(int heads, int tiles_per_head, double l2_bytes_per_head, int 
   g = std::min(g, std::max(1, l2_cap));
   return std::max(1, std::min(g, heads));
 }
+// SM count of the current device (cached per device: one process may drive several GPUs)
 int sm_count() {
-  static int n = 0;  // benign race: idempotent
+  static std::atomic<int> cache[kMaxDevices] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0, v = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-      n = v;
-    if (n <= 0) n = 148;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) n = v;
+    else n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: set it once per (kernel,
+// device) the first time the kernel launches on that device
+cudaError_t ensure_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& pr : done)
+    if (pr.first == kern && pr.second == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(kern, dev);
+  return e;
+}
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
-                     int box_rows) {
+                     int box_rows, bool mn_major) {
+  // fp32 tiles: 32 columns (128 bytes) per box; an MN-major tf32 operand needs the 128-byte
+  // swizzle with 32-byte atoms (the only shared-memory layout the tf32 MMA reads MN-major)
+  if (dtype == TATN_DTYPE_FP32)
+    return make_map_4d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, d, n, H, B, str, box_rows,
+                       mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, 32);
   return make_map_4d(map, tma_dtype(dtype), 2, base, d, n, H, B, str, box_rows);
 }
 }  // namespace tatn_host
@@ -357,20 +415,29 @@ const char* tatn_strerror(int status) {
   }
 }
 
+size_t tatn_fwd_workspace_bytes(const tatn_attn_desc* desc) {
+  if (validate(desc) != TATN_OK) return 0;
+  return kFwdWorkspaceBytes;
+}
+
 int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const void* v, void* o, float* lse,
-             void* stream) {
+             void* workspace, size_t workspace_bytes, void* stream) {
   g_last_launches = 0;
   int st = validate(desc);
   if (st != TATN_OK) return st;
-  if (!q || !k || !v || !o || !lse) return TATN_E_ARG;
+  if (!q || !k || !v || !o || !lse || !workspace) return TATN_E_ARG;
+  if (workspace_bytes < kFwdWorkspaceBytes) return TATN_E_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15u) != 0) return TATN_E_ARG;
   const tatn_attn_desc& d = *desc;
-  const CUtensorMapDataType dt = tma_dtype(d.dtype);
+  const bool in_f32 = d.dtype == TATN_DTYPE_FP32;
+  const bool f32 = in_f32 || d.out_dtype == TATN_OUT_FP32;  // fp32 inputs always give fp32 outputs
   CUtensorMap mq, mk, mv, mo;
-  if (!make_map_4d(&mq, dt, 2, q, d.d, d.Nq, d.H, d.B, d.q_str, 128) ||
-      !make_map_4d(&mk, dt, 2, k, d.d, d.Nk, d.H, d.B, d.k_str, 128) ||
-      !make_map_4d(&mv, dt, 2, v, d.d, d.Nk, d.H, d.B, d.v_str, 128) ||
-      !make_map_4d(&mo, dt, 2, d.out_dtype == TATN_OUT_FP32 ? q : o, d.d, d.Nq, d.H, d.B,
-                   d.out_dtype == TATN_OUT_FP32 ? d.q_str : d.o_str, 128))
+  if (!tatn_host::make_map_4d_ext(&mq, d.dtype, q, d.d, d.Nq, d.H, d.B, d.q_str, 128) ||
+      !tatn_host::make_map_4d_ext(&mk, d.dtype, k, d.d, d.Nk, d.H, d.B, d.k_str, 128) ||
+      !tatn_host::make_map_4d_ext(&mv, d.dtype, v, d.d, d.Nk, d.H, d.B, d.v_str, 128, /*mn_major=*/in_f32))
+    return TATN_E_CUDA;
+  // 16-bit O is stored by TMA (d = 64); the fp32 modes write O from registers (map unused)
+  if (!in_f32 && !tatn_host::make_map_4d_ext(&mo, d.dtype, f32 ? q : o, d.d, d.Nq, d.H, d.B, f32 ? d.q_str : d.o_str, 128))
     return TATN_E_CUDA;
   tatn_dev::FwdParams p{};
   p.B = d.B;
@@ -389,7 +456,6 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.group = 1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
-  const bool f32 = d.out_dtype == TATN_OUT_FP32;
   p.o_f32 = f32 ? static_cast<float*>(o) : nullptr;
   p.o16 = f32 ? nullptr : o;
   p.o_sb = d.o_str[0];
@@ -401,30 +467,41 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   p.k_off = d.k_offset;
   const bool drop = d.p_drop > 0.0;
   set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
-  const int sel = (d.d == 128 ? 8 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 4 : 0) + (f32 ? 2 : 0) + (drop ? 1 : 0);
+  int* ctr = static_cast<int*>(workspace);
   e = cudaErrorInvalidValue;
   cudaEvent_t prof_stop = prof_begin(0, s);
+  if (in_f32) {
+    const int sel = (d.d == 128 ? 2 : 0) + (drop ? 1 : 0);
+    switch (sel) {
+      case 0: e = launch_fwd_tf32<64, false>(mq, mk, mv, p, s); break;
+      case 1: e = launch_fwd_tf32<64, true>(mq, mk, mv, p, s); break;
+      case 2: e = launch_fwd_tf32<128, false>(mq, mk, mv, p, s); break;
+      case 3: e = launch_fwd_tf32<128, true>(mq, mk, mv, p, s); break;
+    }
+  } else {
+    const int sel = (d.d == 128 ? 8 : 0) + (d.dtype == TATN_DTYPE_BF16 ? 4 : 0) + (f32 ? 2 : 0) + (drop ? 1 : 0);
 #define TATN_FWD_CASE(i, DD, B16, F32, DR) \
-  case i: e = launch_fwd<DD, B16, F32, DR>(mq, mk, mv, mo, p, s); break;
-  switch (sel) {
-    TATN_FWD_CASE(0, 64, false, false, false)
-    TATN_FWD_CASE(1, 64, false, false, true)
-    TATN_FWD_CASE(2, 64, false, true, false)
-    TATN_FWD_CASE(3, 64, false, true, true)
-    TATN_FWD_CASE(4, 64, true, false, false)
-    TATN_FWD_CASE(5, 64, true, false, true)
-    TATN_FWD_CASE(6, 64, true, true, false)
-    TATN_FWD_CASE(7, 64, true, true, true)
-    TATN_FWD_CASE(8, 128, false, false, false)
-    TATN_FWD_CASE(9, 128, false, false, true)
-    TATN_FWD_CASE(10, 128, false, true, false)
-    TATN_FWD_CASE(11, 128, false, true, true)
-    TATN_FWD_CASE(12, 128, true, false, false)
-    TATN_FWD_CASE(13, 128, true, false, true)
-    TATN_FWD_CASE(14, 128, true, true, false)
-    TATN_FWD_CASE(15, 128, true, true, true)
-  }
+  case i: e = launch_fwd<DD, B16, F32, DR>(mq, mk, mv, mo, p, ctr, s); break;
+    switch (sel) {
+      TATN_FWD_CASE(0, 64, false, false, false)
+      TATN_FWD_CASE(1, 64, false, false, true)
+      TATN_FWD_CASE(2, 64, false, true, false)
+      TATN_FWD_CASE(3, 64, false, true, true)
+      TATN_FWD_CASE(4, 64, true, false, false)
+      TATN_FWD_CASE(5, 64, true, false, true)
+      TATN_FWD_CASE(6, 64, true, true, false)
+      TATN_FWD_CASE(7, 64, true, true, true)
+      TATN_FWD_CASE(8, 128, false, false, false)
+      TATN_FWD_CASE(9, 128, false, false, true)
+      TATN_FWD_CASE(10, 128, false, true, false)
+      TATN_FWD_CASE(11, 128, false, true, true)
+      TATN_FWD_CASE(12, 128, true, false, false)
+      TATN_FWD_CASE(13, 128, true, false, true)
+      TATN_FWD_CASE(14, 128, true, true, false)
+      TATN_FWD_CASE(15, 128, true, true, true)
+    }
 #undef TATN_FWD_CASE
+  }
   if (prof_stop) cudaEventRecord(prof_stop, s);
   if (e != cudaSuccess) return TATN_E_CUDA;
   g_last_launches = 1;
@@ -451,6 +528,21 @@ int tatn_bwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   if (st != TATN_OK) return st;
   if (!q || !k || !v || !o || !dO || !lse || !dq || !dk || !dv || !workspace) return TATN_E_ARG;
   if (workspace_bytes < tatn_bwd_workspace_bytes(desc)) return TATN_E_WORKSPACE;
+  if (desc->dtype == TATN_DTYPE_FP32) {
+    const int sel = (desc->d == 128 ? 2 : 0) + (desc->p_drop > 0.0 ? 1 : 0);
+    cudaError_t e = cudaErrorInvalidValue;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int n = 0;
+    switch (sel) {
+      case 0: e = launch_bwd_tf32<64, false>(*desc, q, k, v, o, dO, lse, dq, dk, dv, workspace, s, &n); break;
+      case 1: e = launch_bwd_tf32<64, true>(*desc, q, k, v, o, dO, lse, dq, dk, dv, workspace, s, &n); break;
+      case 2: e = launch_bwd_tf32<128, false>(*desc, q, k, v, o, dO, lse, dq, dk, dv, workspace, s, &n); break;
+      case 3: e = launch_bwd_tf32<128, true>(*desc, q, k, v, o, dO, lse, dq, dk, dv, workspace, s, &n); break;
+    }
+    if (e != cudaSuccess) return TATN_E_CUDA;
+    g_last_launches = n;
+    return TATN_OK;
+  }
   return tatn_bwd_launch(*desc, q, k, v, o, dO, lse, dq, dk, dv, workspace, static_cast<cudaStream_t>(stream),
                          &g_last_launches);
 }

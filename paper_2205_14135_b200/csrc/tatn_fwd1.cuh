@@ -1,7 +1,7 @@
 // tatn_fwd1.cuh — persistent FlashAttention forward for d = 64 (kernel K1, one Q tile per item).
 //
-// Same algorithm as tatn_fwd_kernel<64, .., NQ = 1> (Algorithm 2 of the paper, PAPER.md:1239-1271;
-// reference flash.hpp:43-67), restructured as a persistent kernel: two CTAs per SM each loop
+// Algorithm 2 of the paper (reference flash.hpp:43-67) as a persistent
+// kernel: two CTAs per SM each loop
 // over work items (one 128-row Q tile of one head) claimed from a device counter, so the fixed
 // per-tile costs — launch, barrier / TMEM setup, the Q and first K/V load latency, the O
 // epilogue — overlap the previous item's softmax instead of idling the SM:
@@ -17,10 +17,6 @@
 #pragma once
 
 #include "tatn_fwd.cuh"
-
-#ifndef TATN_FWD1_CHUNK_SKIP
-#define TATN_FWD1_CHUNK_SKIP 0  // 1: skip all-masked 32-column chunks of masked tiles (spills at 168 regs: slower)
-#endif
 
 namespace tatn_dev {
 
@@ -51,10 +47,7 @@ __device__ __forceinline__ void fwd1_item(const FwdParams& p, int w, int& bh, in
   qt = (p.mask_kind == kMaskCausal && p.grid == nullptr) ? (p.n_pairs - 1 - slot) : slot;
 }
 
-#ifndef TATN_FWD1_WIDE
-#define TATN_FWD1_WIDE 0  // 1: 256 threads (2 idle warps) so setmaxnreg can move registers to the softmax
-#endif
-constexpr int kFwd1Threads = TATN_FWD1_WIDE ? 256 : 192;
+constexpr int kFwd1Threads = 192;
 
 template <bool BF16, bool OUT_F32, bool DROP>
 __global__ void __launch_bounds__(kFwd1Threads, 2)
@@ -104,11 +97,6 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-#if TATN_FWD1_WIDE
-  // two full warpgroups: softmax 0-3 (setmaxnreg.inc in its branch), producer / MMA / two idle
-  // warps give registers back here
-  if (warp >= 4) setmaxnreg_dec<56>();
-#endif
 
   // per-item schedule (identical in every role)
   struct Item {
@@ -346,9 +334,6 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
     }
     sync_q(n_taken - 1);  // trailing items without tiles: consume their QFull phases
   } else if (warp < 4) {
-#if TATN_FWD1_WIDE
-    setmaxnreg_inc<200>();
-#endif
     // ------------------------------------------------------------ softmax + epilogue warpgroup
     const int row = warp * 32 + lane;  // row within the tile == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
@@ -418,24 +403,15 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
         }
         auto step = [&](auto masked_t) {
           constexpr bool kMasked = decltype(masked_t)::value;
-          // Masked tiles: `lim` grows with the row, so 32-column chunks at or past the warp's
-          // last row's limit are masked for all 32 rows — warp-uniformly skipped (P = 0, no
-          // exponentials): on a causal diagonal tile warp w computes w + 1 chunks, not 4.
-          int hi = 4;  // chunks [hi, 4) are all-masked for this warp
-          if constexpr (kMasked && TATN_FWD1_CHUNK_SKIP) {
-            hi = (max(__shfl_sync(0xffffffffu, lim, 31), 0) + 31) >> 5;
-          }
           if constexpr (kMasked) {
 #pragma unroll
             for (int c = 0; c < 4; ++c)
-              if (c < hi)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) sv[c][i] = (c * 32 + i >= lim) ? __float_as_uint(-INFINITY) : sv[c][i];
+              for (int i = 0; i < 32; ++i) sv[c][i] = (c * 32 + i >= lim) ? __float_as_uint(-INFINITY) : sv[c][i];
           }
           float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (!kMasked || c < hi)
 #pragma unroll
               for (int i = 0; i < 32; i += 4) {
                 mx0 = fmax3(mx0, __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
@@ -469,10 +445,6 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t pk[16];
-            if (kMasked && c >= hi) {
-#pragma unroll
-              for (int k = 0; k < 16; ++k) pk[k] = 0u;
-            } else
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
               const int i = c * 16 + k;

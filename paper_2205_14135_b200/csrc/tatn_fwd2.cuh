@@ -444,28 +444,21 @@ __global__ void __launch_bounds__(384, 1)
                 const uint64_t x =
                     f2_fma(f2_pack(__uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1])), sl2x2, negm);
                 uint64_t pv;
-                if constexpr (TATN_EX2_16 && !OUT_F32 && !DROP) {
+                if (kEmu && (i & 7) < kEmuPairsD<D>) {
+                  pv = exp2_poly_f2(x);
+                } else {
                   float x0, x1;
                   f2_unpack(x, x0, x1);
-                  pk[k] = ex2_pair16<BF16>(x0, x1);
-                  pv = widen_pair16<BF16>(pk[k]);  // l sums exactly the P the MMA consumes
-                } else {
-                  if (kEmu && (i & 7) < kEmuPairsD<D>) {
-                    pv = exp2_poly_f2(x);
-                  } else {
-                    float x0, x1;
-                    f2_unpack(x, x0, x1);
-                    pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
-                  }
-                  float p0, p1;
-                  f2_unpack(pv, p0, p1);
-                  if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
-                    const int j0 = p.k_off + k0 + c * 32 + 2 * k;  // global key index
-                    p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
-                    p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
-                  }
-                  pk[k] = pack2<BF16>(p0, p1);
+                  pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
                 }
+                float p0, p1;
+                f2_unpack(pv, p0, p1);
+                if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
+                  const int j0 = p.k_off + k0 + c * 32 + 2 * k;  // global key index
+                  p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
+                  p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
+                }
+                pk[k] = pack2<BF16>(p0, p1);
                 if (k & 1) rsum1 = f2_add(rsum1, pv);
                 else rsum0 = f2_add(rsum0, pv);
               }

@@ -58,6 +58,9 @@ struct BwdParams {
   int custom_t_words;        // Nq_pad / 32
   int custom_t_b;            // 1: one mask per batch element (b), 0: shared
   int k_off;                 // global index of key 0 (sequence-parallel key shards; multiple of 128)
+  const uint32_t* custom;    // Custom mask as given (tf32 check mode reads it untransposed)
+  int custom_words;
+  int64_t custom_bstride;
 };
 
 }  // namespace tatn_dev

@@ -5,7 +5,8 @@
 //
 // Per call (one head, fp64 n x d matrices):
 //   * validate like the reference (AttnConfig::validate, shape / plan / mask checks);
-//   * round Q, K, V (and dO) to 16 bits with round-to-nearest-even, zero-pad d
+//   * round Q, K, V (and dO) to the device input type — bf16 (default) or fp16 with
+//     round-to-nearest-even, or fp32 (the tf32 check mode, set_input_dtype) — and zero-pad d
 //     to 64 or 128 (zero columns change neither QK^T nor the live O columns);
 //   * run tatn_fwd / tatn_bwd with fp32 outputs (no output rounding);
 //   * return O and the stats as (m = LSE, l = 1) — the same (m, l) pair up to
@@ -37,8 +38,15 @@
 namespace tatn {
 namespace b200 {
 
-// Input rounding dtype for the device path (default bf16; fp16 keeps 3 more mantissa bits).
+// Input dtype of the device path: bf16 (default), fp16 (3 more mantissa bits) or fp32 (inputs
+// kept at binary32 and multiplied as tf32 on the tensor cores: the closest the device gets to
+// the reference's binary64).
 static int g_input_dtype = TATN_DTYPE_BF16;
+void set_input_dtype(int dtype) {
+  if (dtype != TATN_DTYPE_BF16 && dtype != TATN_DTYPE_FP16 && dtype != TATN_DTYPE_FP32)
+    throw std::invalid_argument("tatn b200: input dtype must be TATN_DTYPE_BF16, _FP16 or _FP32");
+  g_input_dtype = dtype;
+}
 void set_input_dtype_fp16(bool fp16) { g_input_dtype = fp16 ? TATN_DTYPE_FP16 : TATN_DTYPE_BF16; }
 
 namespace {
@@ -121,6 +129,19 @@ void upload32(const Matrix& m, int dp, void* dev) {
   for (std::size_t i = 0; i < m.rows(); ++i)
     for (std::size_t j = 0; j < m.cols(); ++j) h[i * dp + j] = static_cast<float>(m(i, j));
   check_cuda(cudaMemcpy(dev, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "upload");
+}
+
+// an input matrix in the device input dtype (fp32: RNE to binary32; else 16-bit RNE)
+std::size_t in_bytes(int dtype) { return dtype == TATN_DTYPE_FP32 ? 4 : 2; }
+void upload_in(const Matrix& m, int dp, int dtype, void* dev) {
+  if (dtype == TATN_DTYPE_FP32) {
+    for (std::size_t i = 0; i < m.rows(); ++i)
+      for (std::size_t j = 0; j < m.cols(); ++j)
+        if (!std::isfinite(static_cast<float>(m(i, j)))) throw std::invalid_argument("tatn b200: non-finite input");
+    upload32(m, dp, dev);
+  } else {
+    upload16(m, dp, dtype, dev);
+  }
 }
 
 Matrix download32(const void* dev, std::size_t rows, std::size_t cols, int dp) {
@@ -284,10 +305,12 @@ FlashSaved forward_impl(const char* op, const Matrix& q, const Matrix& k, const 
     throw std::invalid_argument(std::string(op) + ": bmask block sizes do not match the plan");
   Problem P = make_problem(q, k, cfg);
   const size_t eq = P.n * P.dp, ek = P.nk * P.dp;
-  DevBuf dq(eq * 2), dk(ek * 2), dv(ek * 2), dout(eq * 4), dlse(P.n * 4), dvl(4);
-  upload16(q, P.dp, P.desc.dtype, dq.p);
-  upload16(k, P.dp, P.desc.dtype, dk.p);
-  upload16(v, P.dp, P.desc.dtype, dv.p);
+  const std::size_t es = in_bytes(P.desc.dtype);
+  DevBuf dq(eq * es), dk(ek * es), dv(ek * es), dout(eq * 4), dlse(P.n * 4), dvl(4), fws(16);
+  upload_in(q, P.dp, P.desc.dtype, dq.p);
+  upload_in(k, P.dp, P.desc.dtype, dk.p);
+  upload_in(v, P.dp, P.desc.dtype, dv.p);
+  check_cuda(cudaMemset(fws.p, 0, 16), "zero forward workspace");
   if (cfg.mask.kind == MaskKind::KeyPadding) {
     const int32_t vl = static_cast<int32_t>(std::min<std::size_t>(cfg.mask.valid_len, 0x7fffffff));
     check_cuda(cudaMemcpy(dvl.p, &vl, 4, cudaMemcpyHostToDevice), "upload valid_len");
@@ -317,7 +340,7 @@ FlashSaved forward_impl(const char* op, const Matrix& q, const Matrix& k, const 
       check_cuda(cudaMemcpy(dsub.p, sub.data(), sub.size(), cudaMemcpyHostToDevice), "upload grid prefix");
       d.block_grid = static_cast<const uint8_t*>(dsub.p);
     }
-    check_status(tatn_fwd(&d, dq.p, dk.p, dv.p, dout.p, static_cast<float*>(dlse.p), nullptr), op);
+    check_status(tatn_fwd(&d, dq.p, dk.p, dv.p, dout.p, static_cast<float*>(dlse.p), fws.p, 16, nullptr), op);
     check_cuda(cudaDeviceSynchronize(), op);
     std::vector<float> lse(P.n);
     check_cuda(cudaMemcpy(lse.data(), dlse.p, P.n * 4, cudaMemcpyDeviceToHost), "download lse");
@@ -373,12 +396,13 @@ Gradients backward_impl(const char* op, const FlashSaved& saved, const Matrix& q
     throw std::invalid_argument(std::string(op) + ": bmask block sizes do not match the plan");
   Problem P = make_problem(q, k, cfg);
   const size_t eq = P.n * P.dp, ek = P.nk * P.dp;
-  DevBuf dq(eq * 2), dk(ek * 2), dv(ek * 2), ddo(eq * 2), dov(eq * 4), dlse(P.n * 4), dvl(4);
+  const std::size_t es = in_bytes(P.desc.dtype);
+  DevBuf dq(eq * es), dk(ek * es), dv(ek * es), ddo(eq * es), dov(eq * 4), dlse(P.n * 4), dvl(4);
   DevBuf gq(eq * 4), gk(ek * 4), gv(ek * 4);
-  upload16(q, P.dp, P.desc.dtype, dq.p);
-  upload16(k, P.dp, P.desc.dtype, dk.p);
-  upload16(v, P.dp, P.desc.dtype, dv.p);
-  upload16(d_o, P.dp, P.desc.dtype, ddo.p);
+  upload_in(q, P.dp, P.desc.dtype, dq.p);
+  upload_in(k, P.dp, P.desc.dtype, dk.p);
+  upload_in(v, P.dp, P.desc.dtype, dv.p);
+  upload_in(d_o, P.dp, P.desc.dtype, ddo.p);
   upload32(saved.o, P.dp, dov.p);  // fp32 O: D_i = dO_i . O_i without output rounding
   std::vector<float> lse(P.n);
   for (std::size_t i = 0; i < P.n; ++i)

@@ -4,10 +4,11 @@ Run in the container that has /root/reference (after `make -C oracle`):
     python tests/golden/make_golden.py
 The fixtures are committed; nothing at test time needs /root/reference.
 
-attn_golden.npz holds, per case, the 16-bit inputs (raw uint16 bit patterns of
+attn_golden.npz holds, per case, the inputs (16-bit cases: raw uint16 bit patterns of
 the RNE-rounded N(0,1) inputs from tatn::gaussian_matrix with the SURVEY §8(d)
-seeds) and the reference's fp64 standard_forward / standard_backward outputs
-(reference.cpp:39-204) on those rounded inputs, stored as fp32.
+seeds; fp32 cases — the tf32 check mode, BASELINE configs[0] — the inputs rounded to
+binary32, stored as float32) and the reference's fp64 standard_forward /
+standard_backward outputs (reference.cpp:39-204) on those rounded inputs, stored as fp32.
 Block-sparse cases run the reference's standard path with the block grid
 composed into a Custom additive mask (compose_block_mask, block_mask.hpp:42-46).
 """
@@ -31,6 +32,11 @@ CASES = [
     ("sparse_emptyrow_causal_bf16_d64", 1, 1, 384, 384, 64, "bf16", "causal", None, "emptyrow"),
     # dropout p = 0.2, seed 1234 (slice (b, h) uses seed + b*H + h, the C ABI's batched convention)
     ("dropout_causal_bf16_d64", 1, 2, 192, 192, 64, "bf16", "causal", None, None),
+    # fp32 inputs (ABI v4 tf32 check mode): C1 itself (B=2 H=4 N=512 d=64 non-causal fp32) and two
+    # masked / ragged shapes
+    ("c1_fp32_d64", 2, 4, 512, 512, 64, "fp32", "none", None, None),
+    ("causal_fp32_d128_ragged", 1, 2, 200, 200, 128, "fp32", "causal", None, None),
+    ("padding_fp32_d64", 2, 1, 300, 300, 64, "fp32", "key_padding", [250, 17], None),
 ]
 DROPOUT = {"dropout_causal_bf16_d64": (0.2, 1234)}
 
@@ -48,6 +54,8 @@ def grid_for(kind, tr, tc):
 
 
 def bits16(x, dtype):
+    if dtype == "fp32":  # stored as float32 values
+        return x.astype(np.float32)
     if dtype == "fp16":
         return x.astype(np.float16).view(np.uint16)
     f = x.astype(np.float32)  # already bf16-exact

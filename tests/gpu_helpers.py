@@ -8,11 +8,18 @@ import torch
 from oracle import oracle as O
 from paper_2205_14135_b200 import attention as A
 
-TORCH_DT = {"bf16": torch.bfloat16, "fp16": torch.float16}
+TORCH_DT = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
 
 # north star (BASELINE.json): 16-bit inputs, fp64 oracle on the same rounded inputs
 MAX_ABS = 2e-2
 REL_L2 = 1e-2
+# fp32-input check mode (inputs, P and dS rounded to tf32 on chip, tf32 MMAs, fp32 outputs), fp64
+# oracle on the same fp32 inputs: "tighter for an fp32-input check mode" — 10x the 16-bit bar.
+# At C1 (N(0,1) inputs, |outputs| < 1) max abs <= 2e-3 holds as is; shapes that drive outputs past
+# 1 (a few visible keys: |dV| ~ 10) scale the max-abs bar by max(1, max|ref|) (tf32 keeps a
+# relative precision of 2^-11)
+F32_MAX_ABS = 2e-3
+F32_REL_L2 = 1e-3
 
 
 def make_inputs(B, H, Nq, Nk, d, dtype):
@@ -49,7 +56,7 @@ def run_gpu(q, k, v, do, dtype, mask="none", valid_len=None, grid=None, backward
     if visited:
         vis_f = torch.zeros((tr * tc + 31) // 32, dtype=torch.int32, device="cuda")
         spec.visited = vis_f
-    odt = torch.float32 if out_fp32 else None
+    odt = torch.float32 if (out_fp32 or dtype == "fp32") else None
     o = empty_like_layout(qd, odt)
     o, lse = A.flash_fwd(qd, kd, vd, spec, out=o)
     assert A.last_launch_count() == 1
@@ -61,7 +68,7 @@ def run_gpu(q, k, v, do, dtype, mask="none", valid_len=None, grid=None, backward
         dod = to_dev(do, dtype, layout)
         dq, dk, dv = empty_like_layout(qd, odt), empty_like_layout(kd, odt), empty_like_layout(vd, odt)
         A.flash_bwd(qd, kd, vd, o, dod, lse, spec, dq=dq, dk=dk, dv=dv)
-        assert A.last_launch_count() == (4 if mask == "custom" else 3)
+        assert A.last_launch_count() == (4 if (mask == "custom" and dtype != "fp32") else 3)
         out.update(dq=dq.double().cpu().numpy(), dk=dk.double().cpu().numpy(), dv=dv.double().cpu().numpy())
     torch.cuda.synchronize()
     if visited:
@@ -77,7 +84,9 @@ def bitmap_to_grid(bm: torch.Tensor, tr: int, tc: int) -> np.ndarray:
     return bits.reshape(tr, tc).astype(np.uint8)
 
 
-def assert_close(name, got, ref, max_abs=MAX_ABS, rel_l2=REL_L2):
+def assert_close(name, got, ref, max_abs=MAX_ABS, rel_l2=REL_L2, scale_max_abs=False):
+    """max |got - ref| <= max_abs (times max(1, max|ref|) when scale_max_abs) and
+    ||got - ref||_2 / ||ref||_2 <= rel_l2."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape, (name, got.shape, ref.shape)
@@ -90,6 +99,8 @@ def assert_close(name, got, ref, max_abs=MAX_ABS, rel_l2=REL_L2):
     assert np.all(np.isfinite(got)), f"{name}: non-finite values"
     err = np.abs(got - ref)
     mx = float(err.max()) if err.size else 0.0
+    if scale_max_abs and ref.size:
+        max_abs = max_abs * max(1.0, float(np.abs(ref).max()))
     denom = float(np.linalg.norm(ref))
     rel = float(np.linalg.norm(got - ref) / denom) if denom > 0 else float(np.linalg.norm(got - ref))
     assert mx <= max_abs, f"{name}: max abs err {mx:.3e} > {max_abs}"

@@ -40,7 +40,7 @@ def test_exports_have_c_linkage():
 
 def test_abi_version_and_strerror():
     lib = _lib.load()
-    assert lib.tatn_abi_version() == 3
+    assert lib.tatn_abi_version() == 4
     for code in range(7):
         assert _lib.strerror(code)
     assert _lib.strerror(99) == "unknown status"
@@ -67,6 +67,28 @@ def validate(d):
 def test_valid_descriptor_passes():
     assert validate(good_desc()) == _lib.TATN_OK
     assert validate(good_desc(d=128, dtype=_lib.TATN_DTYPE_FP16, mask_kind=_lib.TATN_MASK_CAUSAL)) == _lib.TATN_OK
+    # ABI v4: fp32 inputs select the tf32 check mode
+    assert validate(good_desc(dtype=_lib.TATN_DTYPE_FP32)) == _lib.TATN_OK
+    assert validate(good_desc(d=128, dtype=_lib.TATN_DTYPE_FP32, out_dtype=_lib.TATN_OUT_FP32)) == _lib.TATN_OK
+
+
+def test_forward_workspace():
+    """ABI v4: the forward's work-item counter lives in a caller-owned 16-byte workspace (no
+    global state in the library); too small / misaligned / missing workspaces are rejected
+    before any device access."""
+    lib = _lib.load()
+    d = good_desc()
+    assert lib.tatn_fwd_workspace_bytes(ctypes.byref(d)) == 16
+    assert lib.tatn_fwd_workspace_bytes(ctypes.byref(good_desc(B=0))) == 0
+    buf = (ctypes.c_uint8 * 64)()
+    base = (ctypes.addressof(buf) + 15) // 16 * 16
+    one = ctypes.c_void_p(base)  # never dereferenced: the calls fail validation first
+    st = lib.tatn_fwd(ctypes.byref(d), one, one, one, one, one, None, 16, None)
+    assert st == _lib.TATN_E_ARG
+    st = lib.tatn_fwd(ctypes.byref(d), one, one, one, one, one, base, 8, None)
+    assert st == _lib.TATN_E_WORKSPACE
+    st = lib.tatn_fwd(ctypes.byref(d), one, one, one, one, one, base + 4, 16, None)
+    assert st == _lib.TATN_E_ARG
 
 
 @pytest.mark.parametrize(
@@ -138,3 +160,19 @@ def test_custom_mask_descriptor():
     assert lib.tatn_bwd_workspace_bytes(ctypes.byref(ok)) == base_ws + 300 * 12 * 4
     per_b = good_desc(mask_kind=3, custom_mask=base, custom_words=12, custom_bstride=3600)
     assert lib.tatn_bwd_workspace_bytes(ctypes.byref(per_b)) == base_ws + 2 * 300 * 12 * 4
+
+
+def test_custom_mask_width_covers_key_offset():
+    """The kernels read word (k_offset + j) / 32 of each row: a key shard at k_offset needs
+    4 * ceil((k_offset + Nk) / 128) words, not ceil(Nk / 32) (advisor finding, round 1)."""
+    buf = (ctypes.c_uint32 * (1024 * 32 + 4))()
+    base = (ctypes.addressof(buf) + 15) // 16 * 16
+    kw = dict(B=1, H=1, Nq=1024, Nk=128, tr=8, tc=1, mask_kind=3, custom_mask=base)
+    d = good_desc(**kw, k_offset=768, custom_words=4)
+    for name in ("q_str", "k_str", "v_str", "o_str"):
+        getattr(d, name)[:] = (1024 * 64, 1024 * 64, 64)
+    assert validate(d) == _lib.TATN_E_MASK
+    d.custom_words = 28  # 4 * ceil((768 + 128) / 128)
+    assert validate(d) == _lib.TATN_OK
+    d.custom_bstride = 1024 * 4  # a per-batch stride must hold Nq rows of the full width
+    assert validate(d) == _lib.TATN_E_MASK

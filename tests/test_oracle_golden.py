@@ -22,6 +22,8 @@ def load_cases():
 
 
 def decode16(bits, dtype):
+    if dtype == "fp32":  # fp32 cases store the float32 values themselves
+        return np.asarray(bits, dtype=np.float32).astype(np.float64)
     bits = np.asarray(bits, dtype=np.uint16)
     if dtype == "fp16":
         return bits.view(np.float16).astype(np.float64)
@@ -55,7 +57,10 @@ def test_generator_matches_golden_seeds():
             assert np.array_equal(O.gaussian_matrix(8, 8, seed), g[key])
 
 
-@pytest.mark.parametrize("idx", range(7))
+N_CASES = len(load_cases()[1])
+
+
+@pytest.mark.parametrize("idx", range(N_CASES))
 def test_oracle_matches_golden(idx):
     z, meta = load_cases()
     m = meta[idx]
