@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 from typing import Optional
 
 import torch
@@ -57,7 +57,11 @@ class AttnSpec:
     tau: Optional[float] = None
     mask: str = "none"
     valid_len: Optional[torch.Tensor] = None  # int32 [B] on device (key_padding)
-    block_grid: Optional[torch.Tensor] = None  # uint8 [tr, tc] on device, 128x128 blocks
+    # block-sparse grid (tatn::BlockMask::grid, block_mask.hpp:14-24): uint8 [tr, tc] on the device over
+    # blocks of block_size = (br, bc) rows x keys — any block size, e.g. the reference's default plan
+    # (64, 256) at N = 1024, d = 64; (128, 128) is the kernels' native tile (no lowering)
+    block_grid: Optional[torch.Tensor] = None
+    block_size: tuple = (128, 128)
     visited: Optional[torch.Tensor] = None  # int32 [ceil(tr*tc/32)] on device, zeroed by caller
     out_fp32: bool = False  # write O / dQ / dK / dV in fp32 (no output rounding)
     p_drop: float = 0.0  # dropout probability in [0, 1) (reference's positional PRNG, dropout.cpp)
@@ -89,6 +93,91 @@ def _check_vec(t, name, dtype, n, device):
                          f"{t.dtype} {tuple(t.shape)} on {t.device}")
 
 
+def _rect_sums(grid: torch.Tensor, br: int, bc: int, Nq: int, Nk: int):
+    """Per 128 x 128 tile (I, J): the number of true blocks overlapping it and the number of blocks
+    overlapping it (2-D prefix sums over the block grid)."""
+    dev = grid.device
+    tr, tc = (Nq + 127) // 128, (Nk + 127) // 128
+    S = torch.zeros((grid.shape[0] + 1, grid.shape[1] + 1), dtype=torch.int64, device=dev)
+    S[1:, 1:] = (grid != 0).to(torch.int64).cumsum(0).cumsum(1)
+    I = torch.arange(tr, device=dev)
+    J = torch.arange(tc, device=dev)
+    r_lo, r_hi = (128 * I) // br, (torch.clamp(128 * I + 128, max=Nq) - 1) // br + 1
+    c_lo, c_hi = (128 * J) // bc, (torch.clamp(128 * J + 128, max=Nk) - 1) // bc + 1
+    rl, rh, cl, ch = r_lo[:, None], r_hi[:, None], c_lo[None, :], c_hi[None, :]
+    true = S[rh, ch] - S[rl, ch] - S[rh, cl] + S[rl, cl]
+    return true, (rh - rl) * (ch - cl)
+
+
+def _block_keep_bits(grid: torch.Tensor, br: int, bc: int, Nq: int, Nk: int) -> torch.Tensor:
+    """Bit-packed element keep matrix [Nq, words] of a block grid: bit j of row i = grid[i // br, j // bc]
+    (compose_block_mask, block_mask.hpp:42-46), built per block row and gathered per query row."""
+    dev = grid.device
+    words = (Nk + 127) // 128 * 4
+    j = torch.arange(words * 32, device=dev)
+    colblk = torch.clamp(j // bc, max=grid.shape[1] - 1)
+    per_blockrow = (grid[:, colblk] != 0) & (j < Nk)[None, :]  # [tr_b, words * 32]
+    bits = per_blockrow.view(grid.shape[0], words, 32).to(torch.int64) << torch.arange(32, device=dev)
+    packed = bits.sum(-1)
+    packed = torch.where(packed >= 2**31, packed - 2**32, packed).to(torch.int32)
+    return packed[torch.arange(Nq, device=dev) // br].contiguous()
+
+
+def _base_keep_bits(spec: "AttnSpec", B: int, Nq: int, Nk: int, device) -> Optional[torch.Tensor]:
+    """The base mask as keep bits [Nq, words] or [B, Nq, words] (None for mask='none')."""
+    words = (Nk + 127) // 128 * 4
+    w0 = torch.arange(words, device=device, dtype=torch.int64) * 32
+    full = (1 << 32) - 1
+
+    def prefix_bits(limit):  # keep keys j < limit (limit broadcast against w0)
+        n = torch.clamp(limit - w0, 0, 32)
+        v = torch.where(n >= 32, torch.full_like(n, full), (torch.ones_like(n) << n) - 1)
+        return torch.where(v >= 2**31, v - 2**32, v).to(torch.int32)
+
+    if spec.mask == "none":
+        return None
+    if spec.mask == "causal":  # keep k_offset + j <= i
+        i = torch.arange(Nq, device=device, dtype=torch.int64)[:, None]
+        return prefix_bits(i + 1 - int(spec.k_offset)).contiguous()
+    if spec.mask == "key_padding":
+        vl = spec.valid_len.to(torch.int64)[:, None, None] - int(spec.k_offset)
+        return prefix_bits(vl).expand(B, Nq, words).contiguous()
+    if spec.mask == "custom":
+        return spec.custom
+    raise ValueError(f"unknown mask kind {spec.mask!r}")
+
+
+def lower_block_mask(spec: "AttnSpec", B: int, Nq: int, Nk: int) -> "AttnSpec":
+    """A block grid at any block size (br, bc) -> the kernels' 128 x 128 tile grid (tile visited iff a
+    true block overlaps it) plus, when some visited tile is only partly covered by true blocks, the
+    blocks' element pattern intersected with the base mask as a Custom keep-bit mask (mask folded
+    in: the result is exactly compose_block_mask(base, grid)). Cached on the spec."""
+    br, bc = (int(x) for x in spec.block_size)
+    if spec.block_grid is None or (br, bc) == (128, 128):
+        return spec
+    ptr = lambda t: t.data_ptr() if t is not None else 0
+    key = (ptr(spec.block_grid), br, bc, B, Nq, Nk, spec.mask, spec.k_offset, ptr(spec.valid_len), ptr(spec.custom))
+    cached = getattr(spec, "_lowered", None)
+    if cached is None or cached[0] != key:  # the lowered grid / bits are cached; the spec's other fields are not
+        g = spec.block_grid
+        if br < 1 or bc < 1 or g.shape[0] * br < Nq or g.shape[1] * bc < Nk:
+            raise ValueError(f"block grid {tuple(g.shape)} x ({br}, {bc}) does not cover Nq={Nq}, Nk={Nk}")
+        true, total = _rect_sums(g, br, bc, Nq, Nk)
+        tiles = (true > 0).to(torch.uint8).contiguous()
+        bits = None
+        if bool(((true > 0) & (true < total)).any()):  # partly covered tiles: element pattern needed
+            bits = _block_keep_bits(g, br, bc, Nq, Nk)
+            base = _base_keep_bits(spec, B, Nq, Nk, g.device)
+            if base is not None:
+                bits = (bits & base).contiguous()
+        cached = (key, tiles, bits)
+        object.__setattr__(spec, "_lowered", cached)
+    _, tiles, bits = cached
+    if bits is None:
+        return replace(spec, block_grid=tiles, block_size=(128, 128))
+    return replace(spec, block_grid=tiles, block_size=(128, 128), mask="custom", custom=bits, valid_len=None)
+
+
 def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttnDesc:
     """Pack a tatn_attn_desc, checking every shape / dtype / device the ABI cannot see (a
     descriptor that disagrees with the buffers would let the kernels read or write out of
@@ -106,6 +195,7 @@ def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttn
         raise ValueError(f"v shape {tuple(v.shape)} != k shape {tuple(k.shape)}")
     if check_o and tuple(o.shape) != tuple(q.shape):
         raise ValueError(f"o shape {tuple(o.shape)} != q shape {tuple(q.shape)}")
+    spec = lower_block_mask(spec, B, Nq, Nk)
     desc = _lib.TatnAttnDesc()
     desc.B, desc.H, desc.Nq, desc.Nk, desc.d = B, H, Nq, Nk, d
     desc.dtype = _dtype_code(q)

@@ -223,6 +223,70 @@ int main() {
       report("blocksparse_empty_row_and_uncovered_keys", empty_ok);
     }
 
+    // ---- block-sparse at the reference's own block sizes: the default plan
+    // (br = 64, bc = 256 at n = 1024, d = 64), br = bc = 16, br = bc = 1 and br = bc = n, against
+    // the reference's standard path under compose_block_mask; all-true at br = 64 == dense
+    {
+      struct BS {
+        const char* name;
+        size_t n, d, br, bc;  // br = bc = 0: the default plan
+        int kind;             // 0 butterfly, 1 local/global, 2 random(0.5), 3 all-true
+        MaskSpec base;
+      };
+      const BS cases[] = {
+          {"bs_default_plan_butterfly_causal", 1024, 64, 0, 0, 0, MaskSpec::causal()},
+          {"bs_16x16_local_global_ragged", 300, 64, 16, 16, 1, MaskSpec::none()},
+          {"bs_1x1_random_padding", 160, 64, 1, 1, 2, MaskSpec::key_padding(150)},
+          {"bs_nxn_single_block", 200, 64, 200, 200, 3, MaskSpec::none()},
+          {"bs_32x64_butterfly_d128", 256, 128, 32, 64, 0, MaskSpec::none()},
+      };
+      for (const BS& c : cases) {
+        AttnConfig cfg = AttnConfig::make(c.n, c.d);
+        cfg.mask = c.base;
+        TileOverrides ov;
+        ov.br = c.br;
+        ov.bc = c.bc;
+        const TilePlan plan = c.br ? plan_tiles(c.n, c.d, 65536, ov) : plan_tiles(c.n, c.d, 65536);
+        BlockMask bm = c.kind == 0   ? make_block_mask_butterfly(plan.tr, plan.tc, plan.br, plan.bc)
+                       : c.kind == 1 ? make_block_mask_local_global(1, 1, plan.tr, plan.tc, plan.br, plan.bc)
+                       : c.kind == 2 ? make_block_mask_random(0.5, 5, plan.tr, plan.tc, plan.br, plan.bc)
+                                     : make_block_mask_random(1.0, 5, plan.tr, plan.tc, plan.br, plan.bc);
+        Matrix q = rounded(gaussian_matrix(c.n, c.d, 81)), k = rounded(gaussian_matrix(c.n, c.d, 82)),
+               v = rounded(gaussian_matrix(c.n, c.d, 83)), dO = rounded(gaussian_matrix(c.n, c.d, 84));
+        MemoryModel mf(plan.m_capacity), mb(plan.m_capacity);
+        FlashSaved sb = blocksparse_forward(q, k, v, cfg, plan, bm, mf);
+        Gradients g = blocksparse_backward(sb, q, k, v, dO, bm, mb);
+        AttnConfig ccfg = cfg;
+        ccfg.mask = compose_block_mask(cfg.mask, bm, c.n);
+        ForwardArtifacts rb = standard_forward(q, k, v, ccfg);
+        Gradients rg = standard_backward(rb, q, k, v, dO, ccfg);
+        const std::string tag = std::string(c.name) + "_br" + std::to_string(plan.br) + "_bc" + std::to_string(plan.bc);
+        report(tag + "_forward", close(sb.o, rb.o), fmt(max_abs(sb.o, rb.o), rel_l2(sb.o, rb.o)));
+        report(tag + "_backward", close(g.dq, rg.dq) && close(g.dk, rg.dk) && close(g.dv, rg.dv),
+               fmt(max_abs(g.dk, rg.dk), rel_l2(g.dk, rg.dk)));
+        const IoPrediction pbs = predict_blocksparse_io(c.n, c.d, plan, bm.density);
+        report(tag + "_counters_closed_form", c.n % plan.br != 0 || c.n % plan.bc != 0 ||
+                                                  (mf.counter().hbm_read_elems == pbs.reads &&
+                                                   mf.counter().hbm_write_elems == pbs.writes));
+      }
+      {  // all-true at br = 64 runs on the exact tile path: bit-identical to the dense engine
+        const size_t n = 512, d = 64;
+        AttnConfig cfg = AttnConfig::make(n, d);
+        cfg.mask = MaskSpec::causal();
+        TileOverrides ov;
+        ov.br = 64;
+        ov.bc = 64;
+        const TilePlan plan = plan_tiles(n, d, 65536, ov);
+        BlockMask all = make_block_mask_random(1.0, 1, plan.tr, plan.tc, plan.br, plan.bc);
+        Matrix q = rounded(gaussian_matrix(n, d, 91)), k = rounded(gaussian_matrix(n, d, 92)),
+               v = rounded(gaussian_matrix(n, d, 93));
+        MemoryModel m1(plan.m_capacity), m2(plan.m_capacity);
+        FlashSaved dense = flash_forward(q, k, v, cfg, plan, m1);
+        FlashSaved sp = blocksparse_forward(q, k, v, cfg, plan, all, m2);
+        report("bs_alltrue_br64_bit_identical_forward", dense.o == sp.o && dense.stats.m == sp.stats.m);
+      }
+    }
+
     // ---- observer: after outer block j the snapshot equals the oracle on the key prefix
     {
       const size_t n = 600, d = 64;
@@ -298,12 +362,8 @@ int main() {
       AttnConfig wcfg = AttnConfig::make(n, 160);
       report("error_head_dim_over_128", throws([&] { flash_forward(wide, wide, wide, wcfg, plan_tiles(n, 160, 116224), mem); }));
       BlockMask b64 = make_block_mask_butterfly(4, 4, 64, 64);
-      TileOverrides ov;
-      ov.br = 64;
-      ov.bc = 64;
-      const TilePlan p64 = plan_tiles(n, d, 65536, ov);
-      report("error_block_size_not_multiple_of_128",
-             throws([&] { blocksparse_forward(x, x, x, ok, p64, b64, mem); }));
+      const TilePlan p128 = plan_tiles(n, d, 65536);
+      report("error_bmask_plan_mismatch", throws([&] { blocksparse_forward(x, x, x, ok, p128, b64, mem); }));
     }
 
     // ---- dropout: same positional mask as the reference (dropout.cpp)

@@ -18,9 +18,12 @@
 // Dropout follows the reference's positional generator bit for bit (the mask at
 // (i, j) is a pure function of (seed, i, j), dropout.hpp:14-30), so forward and
 // backward regenerate identical masks. There is no CPU fallback: unsupported
-// inputs (d > 128, block sizes that are not multiples of 128) throw, and a missing
-// sm_100 device surfaces as std::runtime_error. Custom n x n masks are bit-packed
-// into the ABI's keep matrix.
+// inputs (d > 128) throw, and a missing sm_100 device surfaces as std::runtime_error.
+// Custom n x n masks are bit-packed into the ABI's keep matrix. Block masks of any
+// block size (the plan's br x bc) run on the kernels' 128 x 128 tiles:
+// a tile is visited iff a true block overlaps it, and when br or bc is not a multiple
+// of 128 the blocks' element pattern (compose_block_mask) is applied inside the tiles
+// through the same keep-bit path.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -208,42 +211,73 @@ Problem make_problem(const Matrix& q, const Matrix& k, const AttnConfig& cfg) {
   return P;
 }
 
-// MaskKind::Custom: the n x n additive pattern (0 keep / -inf mask, validated by
-// AttnConfig::validate) bit-packed into the ABI's keep matrix [n][words], words =
-// ceil(nk / 128) * 4, and uploaded; the descriptor points at it for the call's lifetime.
+// Map a BlockMask at the plan's block size (br x bc, any size >= 1) onto the kernels' 128 x 128
+// tile grid: tile (I, J) is visited iff some true block overlaps it. The grid is exact — no
+// element pattern needed inside the tiles — when every visited tile is covered by true blocks
+// only (always so when br and bc are multiples of 128, and for an all-true mask); otherwise
+// CustomMask carries the element pattern of the blocks.
+struct TileGrid {
+  std::vector<uint8_t> g;  // tr x tc at 128 x 128
+  bool exact = true;
+};
+TileGrid tile_grid(const BlockMask& bm, std::size_t n, std::size_t nk) {
+  if (bm.br == 0 || bm.bc == 0)
+    throw std::invalid_argument("blocksparse: bmask block sizes must be positive");
+  if (bm.grid.size() != bm.tr * bm.tc || bm.tr * bm.br < n || bm.tc * bm.bc < nk)
+    throw std::invalid_argument("blocksparse: bmask does not cover the problem");
+  const std::size_t tr = (n + 127) / 128, tc = (nk + 127) / 128;
+  TileGrid t;
+  t.g.assign(tr * tc, 0);
+  std::vector<uint8_t> any_false(tr * tc, 0);
+  for (std::size_t bi = 0; bi < bm.tr; ++bi) {
+    const std::size_t r0 = bi * bm.br;
+    if (r0 >= n) break;
+    const std::size_t r1 = std::min(n, r0 + bm.br) - 1;
+    for (std::size_t bj = 0; bj < bm.tc; ++bj) {
+      const std::size_t c0 = bj * bm.bc;
+      if (c0 >= nk) break;
+      const std::size_t c1 = std::min(nk, c0 + bm.bc) - 1;
+      for (std::size_t I = r0 / 128; I <= r1 / 128; ++I)
+        for (std::size_t J = c0 / 128; J <= c1 / 128; ++J) (bm.at(bi, bj) ? t.g : any_false)[I * tc + J] = 1;
+    }
+  }
+  for (std::size_t x = 0; x < t.g.size(); ++x) t.exact = t.exact && !(t.g[x] && any_false[x]);
+  return t;
+}
+
+// Keep bits for the Custom path: bit-packed [n][words], words = ceil(nk / 128) * 4, uploaded;
+// the descriptor points at it for the call's lifetime. Built when the mask is MaskKind::Custom
+// (the n x n additive pattern, 0 keep / -inf mask, validated by AttnConfig::validate) and when a
+// block mask must be applied per element: then keep(i, j) = !is_masked(base, i, j) and
+// bmask(i / br, j / bc) — exactly compose_block_mask (block_mask.hpp:42-46) — and the call runs
+// as a Custom mask (the base mask's causal / key-padding rule is folded into the bits).
 struct CustomMask {
+  bool on;
   DevBuf buf;
   int32_t words;
-  CustomMask(const AttnConfig& cfg, std::size_t n, std::size_t nk)
-      : buf(cfg.mask.kind == MaskKind::Custom ? n * ((nk + 127) / 128 * 4) * 4 : 0),
+  CustomMask(const AttnConfig& cfg, std::size_t n, std::size_t nk, const BlockMask* bm, bool fine)
+      : on(cfg.mask.kind == MaskKind::Custom || fine),
+        buf(on ? n * ((nk + 127) / 128 * 4) * 4 : 0),
         words(static_cast<int32_t>((nk + 127) / 128 * 4)) {
-    if (cfg.mask.kind != MaskKind::Custom) return;
+    if (!on) return;
     std::vector<uint32_t> bits(n * static_cast<std::size_t>(words), 0u);
     for (std::size_t i = 0; i < n; ++i)
-      for (std::size_t j = 0; j < nk; ++j)
-        if (cfg.mask.custom(i, j) == 0.0) bits[i * words + j / 32] |= 1u << (j % 32);
+      for (std::size_t j = 0; j < nk; ++j) {
+        bool keep = !is_masked(cfg.mask, i, j);
+        if (fine) keep = keep && bm->at(i / bm->br, j / bm->bc);
+        if (keep) bits[i * words + j / 32] |= 1u << (j % 32);
+      }
     check_cuda(cudaMemcpy(buf.p, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice), "upload custom mask");
   }
   void attach(tatn_attn_desc& d) const {
-    if (d.mask_kind != TATN_MASK_CUSTOM) return;
+    if (!on) return;
+    d.mask_kind = TATN_MASK_CUSTOM;
+    d.valid_len = nullptr;  // a key-padding base mask is in the bits
     d.custom_mask = static_cast<const uint32_t*>(buf.p);
     d.custom_words = words;
     d.custom_bstride = 0;
   }
 };
-
-// Expand a BlockMask whose block sizes are multiples of 128 to the kernels' 128 x 128 tile grid.
-std::vector<uint8_t> tile_grid(const BlockMask& bm, std::size_t n, std::size_t nk) {
-  if (bm.br == 0 || bm.bc == 0 || bm.br % 128 != 0 || bm.bc % 128 != 0)
-    throw std::invalid_argument("blocksparse: bmask block sizes must be multiples of 128 on the sm_100a path");
-  if (bm.grid.size() != bm.tr * bm.tc || bm.tr * bm.br < n || bm.tc * bm.bc < nk)
-    throw std::invalid_argument("blocksparse: bmask does not cover the problem");
-  const std::size_t tr = (n + 127) / 128, tc = (nk + 127) / 128;
-  std::vector<uint8_t> g(tr * tc);
-  for (std::size_t i = 0; i < tr; ++i)
-    for (std::size_t j = 0; j < tc; ++j) g[i * tc + j] = bm.at(i * 128 / bm.br, j * 128 / bm.bc) ? 1 : 0;
-  return g;
-}
 
 // ---- MemoryModel charges: the reference's counting rules (io_predict.hpp:12-56),
 // evaluated per (query block, key block) so that ragged shapes, key prefixes and
@@ -316,12 +350,13 @@ FlashSaved forward_impl(const char* op, const Matrix& q, const Matrix& k, const 
     check_cuda(cudaMemcpy(dvl.p, &vl, 4, cudaMemcpyHostToDevice), "upload valid_len");
     P.desc.valid_len = static_cast<const int32_t*>(dvl.p);
   }
-  const CustomMask cmask(cfg, P.n, P.nk);
+  const TileGrid tg = bm ? tile_grid(*bm, P.n, P.nk) : TileGrid{};
+  const CustomMask cmask(cfg, P.n, P.nk, bm, !tg.exact);
   cmask.attach(P.desc);
   std::vector<uint8_t> grid;
   DevBuf dgrid(bm ? ((P.n + 127) / 128) * ((P.nk + 127) / 128) : 0);
   if (bm) {
-    grid = tile_grid(*bm, P.n, P.nk);
+    grid = tg.g;
     check_cuda(cudaMemcpy(dgrid.p, grid.data(), grid.size(), cudaMemcpyHostToDevice), "upload grid");
     P.desc.block_grid = static_cast<const uint8_t*>(dgrid.p);
     P.desc.br = P.desc.bc = 128;
@@ -414,11 +449,12 @@ Gradients backward_impl(const char* op, const FlashSaved& saved, const Matrix& q
     check_cuda(cudaMemcpy(dvl.p, &vl, 4, cudaMemcpyHostToDevice), "upload valid_len");
     P.desc.valid_len = static_cast<const int32_t*>(dvl.p);
   }
-  const CustomMask cmask(cfg, P.n, P.nk);
+  const TileGrid tg = bm ? tile_grid(*bm, P.n, P.nk) : TileGrid{};
+  const CustomMask cmask(cfg, P.n, P.nk, bm, !tg.exact);
   cmask.attach(P.desc);
   DevBuf dgrid(bm ? ((P.n + 127) / 128) * ((P.nk + 127) / 128) : 0);
   if (bm) {
-    const auto grid = tile_grid(*bm, P.n, P.nk);
+    const auto& grid = tg.g;
     check_cuda(cudaMemcpy(dgrid.p, grid.data(), grid.size(), cudaMemcpyHostToDevice), "upload grid");
     P.desc.block_grid = static_cast<const uint8_t*>(dgrid.p);
     P.desc.br = P.desc.bc = 128;

@@ -53,8 +53,9 @@ def test_golden_fixture(cuda_device, idx):
     ref = {key: z[f"{name}/{key}"].astype(np.float64) for key in ("o", "lse", "dq", "dk", "dv")}
     if m["dtype"] == "fp32":
         for key in ("o", "lse", "dq", "dk", "dv"):
-            G.assert_close(key, got[key], ref[key], max_abs=G.F32_MAX_ABS, rel_l2=G.F32_REL_L2,
-                           scale_max_abs=name != "c1_fp32_d64")
+            stress = name != "c1_fp32_d64"  # C1 at the absolute bar, the other fp32 fixtures at the stress bar
+            G.assert_close(key, got[key], ref[key], max_abs=G.F32_MAX_ABS_STRESS if stress else G.F32_MAX_ABS,
+                           rel_l2=G.F32_REL_L2, scale_max_abs=stress)
     else:
         compare_all(got, ref)
     if grid is not None:

@@ -116,3 +116,48 @@ def test_programmatic_dependent_launch_matches_plain_launches(tmp_path):
     for key in ("o", "lse", "dk", "dv"):
         assert torch.equal(res["1"][key], res["0"][key]), key
     assert torch.allclose(res["1"]["dq"], res["0"]["dq"], atol=2e-2, rtol=0)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_many_concurrent_streams_and_graphs_with_eager(cuda_device, d):
+    """ABI v4: the forward's work-item counter is the caller's workspace, so any number of
+    concurrent launches (here 80 streams, more than round 1's 64 global counter slots) plus
+    graph replays interleaved with eager launches on other streams give the reference result
+    (calls may run concurrently with no coordination)."""
+    spec = A.AttnSpec(mask="causal")
+    probs = [_inputs(1, 4, 640, d, seed=100 + i)[:3] for i in range(8)]
+    refs = []
+    for q, k, v in probs:
+        refs.append(A.flash_fwd(q, k, v, spec))
+    torch.cuda.synchronize()
+    # a graph of one forward with its own workspace
+    gq, gk, gv = probs[0]
+    gws = A.fwd_workspace(gq.device)
+    go = torch.empty_like(gq)
+    glse = torch.empty(gq.shape[:3], dtype=torch.float32, device="cuda")
+    A.flash_fwd(gq, gk, gv, spec, out=go, lse=glse, workspace=gws)
+    torch.cuda.synchronize()
+    gs = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=gs):
+        A.flash_fwd(gq, gk, gv, spec, out=go, lse=glse, workspace=gws)
+    streams = [torch.cuda.Stream() for _ in range(80)]
+    wss = [A.fwd_workspace(gq.device) for _ in streams]
+    outs = [None] * len(streams)
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for i, s in enumerate(streams):
+            with torch.cuda.stream(s):
+                q, k, v = probs[i % len(probs)]
+                outs[i] = A.flash_fwd(q, k, v, spec, workspace=wss[i])
+            if i % 16 == 0:
+                with torch.cuda.stream(gs):
+                    graph.replay()
+        torch.cuda.synchronize()
+        for i, (o, lse) in enumerate(outs):
+            ro, rl = refs[i % len(probs)]
+            assert torch.equal(o, ro) and torch.equal(lse, rl), (rep, i)
+        assert torch.equal(go, refs[0][0]) and torch.equal(glse, refs[0][1])
+    # every workspace is back to zero (each launch resets its counter)
+    for w in wss + [gws]:
+        assert int(w.sum()) == 0
