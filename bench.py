@@ -5,11 +5,14 @@
                     [--workload NAME] [--no-sweep] [--no-cpu-baseline]
 
 Our arm (default): one "step" is one forward (K1) + backward (K2-K4) over the
-workload's batch on each GPU, through the C ABI, with inputs resident in HBM.
-Multi-GPU (torchrun, one process per GPU): weak scaling, each rank owns its own
-(b, h) slices of the global batch (no collective on the data path); the timed
-region is bracketed by barrier + synchronize and the max over ranks is taken.
-Rank 0 prints ONE JSON line (value = whole-job TFLOP/s).
+workload's batch, through the C ABI, with inputs resident in HBM.
+Multi-GPU (torchrun, one process per GPU): strong scaling through the launcher —
+the workload's fixed B*H (batch, head) slices are split by
+launcher.BHShardedAttention (rank r runs shard_range(B*H, N, r) as [S, 1, N, d]
+slices; per-slice valid_len keeps key padding exact); no collective on the data
+path; the timed region is bracketed by barrier + synchronize and the max over
+ranks is taken; value = the whole config's FLOPs / that time. Rank 0 prints ONE
+JSON line (value = whole-job TFLOP/s).
 
 --impl reference: the reference's own CPU implementation of the path
 (oracle/_ref = the reference sources compiled here; else the oracle port) on the
@@ -151,7 +154,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ our arm
-def make_inputs(w, device, seed=0):
+def make_inputs(w, device, seed=0, shard=None):
+    """Synthetic N(0,1) q, k, v, dO of the workload on `device`. With a launcher shard
+    (BHShardedAttention) only this rank's slices are built, as [S, 1, N, d]."""
     import numpy as np
     import torch
 
@@ -159,13 +164,15 @@ def make_inputs(w, device, seed=0):
 
     dt = torch.bfloat16 if w["dtype"] == "bf16" else torch.float16
     g = torch.Generator(device=device).manual_seed(seed)
-    shape = (w["B"], w["H"], w["N"], w["d"])
+    shape = (w["B"], w["H"], w["N"], w["d"]) if shard is None else (shard.n_local, 1, w["N"], w["d"])
     q, k, v, do = (torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(dt) for _ in range(4))
     spec = A.AttnSpec(mask=w["mask"])
     if w["mask"] == "key_padding":
-        rng = np.random.default_rng(2124 + seed)  # valid_len ~ U{N-20..N}
-        spec.valid_len = torch.as_tensor(rng.integers(w["N"] - 20, w["N"] + 1, size=w["B"]).astype(np.int32),
-                                         device=device)
+        rng = np.random.default_rng(2124)  # valid_len ~ U{N-20..N}, one per batch element
+        vl = rng.integers(w["N"] - 20, w["N"] + 1, size=w["B"]).astype(np.int32)
+        if shard is not None:  # per slice of this rank's shard
+            vl = np.asarray(shard.local_valid_len(vl), dtype=np.int32)
+        spec.valid_len = torch.as_tensor(vl, device=device)
     if w.get("grid") == "butterfly":
         spec.block_grid = torch.from_numpy(butterfly(w["N"] // 128)).to(device)
     return q, k, v, do, spec
@@ -260,7 +267,11 @@ def run_ours(args, env):
     flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
     flush = lambda: flush_buf.zero_()
 
-    q, k, v, do, spec = make_inputs(w, device, seed=env.rank)
+    from paper_2205_14135_b200.launcher import BHShardedAttention
+
+    # strong scaling: the fixed config's B*H slices split across the ranks by the launcher
+    shard = BHShardedAttention(w["B"], w["H"], env) if env.world > 1 else None
+    q, k, v, do, spec = make_inputs(w, device, seed=env.rank, shard=shard)
     step = Step(q, k, v, do, spec)
     for _ in range(args.warmup):
         step()
@@ -301,8 +312,10 @@ def run_ours(args, env):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     launches_per_step = 1 + 3  # K1 | K2 K3 K4
-    f_fwd, f_bwd = flops(w)
-    total_flops = (f_fwd + f_bwd) * env.world * args.steps
+    f_fwd, f_bwd = flops(w)  # the whole config (all ranks' slices)
+    total_flops = (f_fwd + f_bwd) * args.steps
+    local_slices = shard.n_local if shard is not None else w["B"] * w["H"]
+    lf_fwd, lf_bwd = flops(w, slices=local_slices)  # this rank's share (per-kernel roofline)
     value = total_flops / (ms_max * 1e-3) / 1e12
 
     # ---------------- e2e through the public API with host buffers (pinned), per step:
@@ -390,17 +403,17 @@ def run_ours(args, env):
         slices = w["B"] * w["H"]
         k3_avg = k3_ms / max(k3_n, 1)
         k1_avg = k1_ms / max(k1_n, 1)
-        k3_tf = f_bwd / (k3_avg * 1e-3) / 1e12
-        k1_tf = f_fwd / (k1_avg * 1e-3) / 1e12
+        k3_tf = lf_bwd / (k3_avg * 1e-3) / 1e12
+        k1_tf = lf_fwd / (k1_avg * 1e-3) / 1e12
         traffic, traffic_src = ncu_traffic(args.workload)
         rl = {"kernel": "tatn_bwd_kernel (K3: S^T, dP^T, dV, dK, dQ^T GEMMs)", "bound": "tensor",
               "achieved": round(k3_tf, 2), "peak": peaks["tflops"], "unit": "TFLOP/s",
               "frac": round(k3_tf / peaks["tflops"], 4), "peak_source": peaks["source"] + ", burst bf16",
-              "algorithmic_flops_per_launch": f_bwd, "avg_launch_ms": round(k3_avg, 5), "launches": k3_n,
+              "algorithmic_flops_per_launch": lf_bwd, "avg_launch_ms": round(k3_avg, 5), "launches": k3_n,
               "traffic": traffic, "traffic_source": traffic_src,
-              "io_bound_bytes_theorem2": iomodel.theorem2_bound_bytes(w["N"], w["d"], 2, slices, backward=True)
+              "io_bound_bytes_theorem2": iomodel.theorem2_bound_bytes(w["N"], w["d"], 2, local_slices, backward=True)
               if w.get("grid") is None else None,
-              "compulsory_bytes": iomodel.compulsory_bytes(w["N"], w["d"], 2, slices, backward=True)}
+              "compulsory_bytes": iomodel.compulsory_bytes(w["N"], w["d"], 2, local_slices, backward=True)}
         kernels = {"fwd_K1": {"avg_launch_ms": round(k1_avg, 5), "tflops": round(k1_tf, 2),
                               "frac_of_peak": round(k1_tf / peaks["tflops"], 4), "launches": k1_n},
                    "bwd_K3": {"avg_launch_ms": round(k3_avg, 5), "tflops": round(k3_tf, 2),
@@ -408,13 +421,15 @@ def run_ours(args, env):
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": env.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic N(0,1) q, k, v, dO",
-            "config": {"workload": w["desc"], "model": args.workload, "global_batch": w["B"] * env.world,
+            "scaling": "strong", "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic N(0,1) q, k, v, dO",
+            "config": {"workload": w["desc"], "model": args.workload, "global_batch": w["B"],
                        "heads": w["H"], "seq_len": w["N"], "head_dim": w["d"], "mask": w["mask"],
-                       "parallelism": f"(b,h)-sharded x{env.world}, no collective",
+                       "parallelism": f"(b,h)-sharded x{env.world} by launcher.BHShardedAttention "
+                                      f"({w['B'] * w['H']} slices, <= {-(-w['B'] * w['H'] // env.world)} per GPU), "
+                                      "no collective",
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "launch": "eager" if args.no_graph else "CUDA graph of the step's 4 kernels, replayed per step",
-                       "flops_per_step_per_gpu": f_fwd + f_bwd,
+                       "flops_per_step": f_fwd + f_bwd,
                        "flop_count": "fwd 4*d*P, bwd 10*d*P per slice; P = N(N+1)/2 causal, N^2 otherwise"},
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": round(float(te.item()) / args.steps, 4),
@@ -458,9 +473,10 @@ def run_ours(args, env):
 
 
 # ------------------------------------------------------------------------------ CPU legs (oracle/)
-def _cpu_sample(w, steps=1):
-    """Time the reference's CPU path on a bounded sample: one (b, h) slice per host
-    thread per step. Returns (tflops, seconds, slices, threads, kind, sample text)."""
+def _cpu_sample(w, steps=1, slices=None):
+    """Time the reference's CPU path per step on `slices` (b, h) slices (default: a bounded
+    sample of one slice per host thread), every host thread busy.
+    Returns (tflops, seconds, slices, threads, kind, sample text)."""
     from oracle import oracle as O
 
     threads = os.cpu_count() or 1
@@ -468,7 +484,7 @@ def _cpu_sample(w, steps=1):
     memeff = N >= 8192
     if w.get("grid"):
         mask = "none"  # the reference has no block-sparse engine; time its dense path on the slice shape
-    slices = threads
+    slices = slices or threads
     kind = "reference" if O.have_ref() else "port"
     secs = []
     for _ in range(steps):
@@ -489,9 +505,10 @@ def _cpu_sample(w, steps=1):
     ff, fb = flops(dict(w, grid=None, mask=("causal" if w["mask"] == "causal" else "none")), slices=slices)
     tf = (ff + fb) * steps / sum(secs) / 1e12
     what = ("memeff_forward+memeff_backward" if memeff else "standard_forward+standard_backward")
-    sample = (f"{slices} (b,h) slices of N={N} d={d} mask={mask} per step, reference {what} fp64 "
+    whole = " (the whole batch)" if slices == w["B"] * w["H"] else ""
+    sample = (f"{slices} (b,h) slices{whole} of N={N} d={d} mask={mask} per step, reference {what} fp64 "
               f"({'oracle/_ref: reference sources compiled' if kind == 'reference' else 'oracle C port'}), "
-              f"one std::thread per slice")
+              f"{threads} std::threads, one slice each at a time")
     return tf, sum(secs) / steps, slices, threads, kind, sample
 
 
@@ -506,13 +523,18 @@ def cpu_baseline(w):
 
 def run_reference(args, env):
     w = WORKLOADS[args.workload]
+    # the whole batch per step where the reference's standard path finishes it in a few seconds
+    # (GPT-2 small: 96 slices ~ 2 s on 16 cores), else one slice per host thread
+    threads = os.cpu_count() or 1
+    est_s = (w["B"] * w["H"] / threads) * (w["N"] / 1024) ** 2 * 0.35 * (w["d"] / 64)
+    slices = w["B"] * w["H"] if (w["N"] < 8192 and est_s <= 4.0) else None
     for _ in range(args.warmup):
-        _cpu_sample(w, steps=1)
-    tf, s, slices, threads, kind, sample = _cpu_sample(w, steps=args.steps)
+        _cpu_sample(w, steps=1, slices=slices)
+    tf, s, slices, threads, kind, sample = _cpu_sample(w, steps=args.steps, slices=slices)
     return {
         "impl": "reference", "metric": METRIC, "value": round(tf, 6), "unit": UNIT, "n_gpus": env.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) (tatn::gaussian_matrix)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) (tatn::gaussian_matrix)",
         "config": {"workload": w["desc"], "model": args.workload, "global_batch": w["B"], "heads": w["H"],
                    "seq_len": w["N"], "head_dim": w["d"], "mask": w["mask"],
                    "parallelism": f"host threads x{threads} over (b,h) slices"},

@@ -192,10 +192,13 @@ __global__ void __launch_bounds__(256) tatn_bwd_pre(const void* __restrict__ o_,
       const size_t off = static_cast<size_t>(b) * ob + static_cast<size_t>(h) * oh + static_cast<size_t>(qi) * on + c * 8;
       float of[8], df[8];
       if constexpr (DO_F32) {
+        // tf32 check mode: dP = dO V^T is formed from dO rounded to tf32, so D = rowsum(dO o O)
+        // uses the same rounded dO — then sum_j P_ij (dP_ij - D_i) = 0 holds as in exact arithmetic
+        // (the gradient is exact for the rounded dO instead of carrying its rounding in dS)
         const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(dO_) + off);
         const float4 a0 = src[0], a1 = src[1];
-        df[0] = a0.x; df[1] = a0.y; df[2] = a0.z; df[3] = a0.w;
-        df[4] = a1.x; df[5] = a1.y; df[6] = a1.z; df[7] = a1.w;
+        df[0] = round_tf32(a0.x); df[1] = round_tf32(a0.y); df[2] = round_tf32(a0.z); df[3] = round_tf32(a0.w);
+        df[4] = round_tf32(a1.x); df[5] = round_tf32(a1.y); df[6] = round_tf32(a1.z); df[7] = round_tf32(a1.w);
       } else {
         const uint4 dv = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dO_) + off);
         const uint32_t* dw = reinterpret_cast<const uint32_t*>(&dv);

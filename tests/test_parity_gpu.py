@@ -113,16 +113,17 @@ def test_c4_long_context_n2048_d128_causal(cuda_device):
     compare_all({key: sub(val) for key, val in got.items()}, ref)
 
 
-def test_c4_n16k_sampled_rows_and_identities(cuda_device):
-    # C4 at N=16K (B=1, H=32, d=128 causal): full-size run; sampled query rows
+@pytest.mark.parametrize("N", [4096, 8192, 16384])
+def test_c4_sampled_rows_and_identities(cuda_device, N):
+    # C4 at N = 4K, 8K, 16K (B = 16384/N, H=32, d=128 causal): full-size run; sampled query rows
     # of O, LSE and dQ against the oracle for three heads, and the exact identities
     #   sum_j dK_j = 0  and  sum_j dV_j = sum_i dO_i   (rows of P sum to 1)
-    B, H, N, d = 1, 32, 16384, 128
-    heads = [(0, 0), (0, 17), (0, 31)]
+    B, H, d = 16384 // N, 32, 128
+    heads = [(0, 0), (B - 1, 17), (B // 2, 31)]
     dev, kept = G.make_device_inputs(B, H, N, d, "bf16", keep_heads=heads)
     # fp32 outputs: D = dO.O then uses the unrounded O, as the reference does
     out = G.run_device(dev, "bf16", mask="causal", out_fp32=True)
-    rows = np.array([0, 1, 127, 128, 4095, 8191, 8192, 12345, 16383])
+    rows = np.unique(np.array([0, 1, 127, 128, N // 4 - 1, N // 2 - 1, N // 2, (3 * N) // 4 + 57, N - 1]))
     for (b, h) in heads:
         q, k, v, do = (kept[(b, h, n)] for n in ("q", "k", "v", "do"))
         o_r, lse_r = O.forward_rows(q, k, v, rows, mask="causal")
@@ -133,18 +134,19 @@ def test_c4_n16k_sampled_rows_and_identities(cuda_device):
     G.check_identities(out, dev)
 
 
-def test_c5_butterfly_n16k_visited_and_sampled_rows(cuda_device):
-    # C5: block-sparse FlashAttention, butterfly 128x128 blocks, N=16K, d=64,
-    # B = 65536/N = 4, H = 16. Visited tiles must equal the grid bit-exactly.
-    B, H, N, d = 4, 16, 16384, 64
+@pytest.mark.parametrize("N", [16384, 32768, 65536])
+def test_c5_butterfly_visited_and_sampled_rows(cuda_device, N):
+    # C5: block-sparse FlashAttention, butterfly 128x128 blocks, N = 16K, 32K, 64K (Path-X /
+    # Path-256 shapes), d=64, B = 65536/N, H = 16. Visited tiles must equal the grid bit-exactly.
+    B, H, d = 65536 // N, 16, 64
     tr = N // 128
     grid = O.block_mask_butterfly(tr, tr)
-    heads = [(0, 0), (3, 15)]
+    heads = [(0, 0), (B - 1, 15)]
     dev, kept = G.make_device_inputs(B, H, N, d, "bf16", keep_heads=heads)
     out = G.run_device(dev, "bf16", grid=grid, visited=True, out_fp32=True)
     assert np.array_equal(out["visited_fwd"], grid)
     assert np.array_equal(out["visited_bwd"], grid)
-    rows = np.array([0, 77, 128, 5000, 9999, 16383])
+    rows = np.array([0, 77, 128, 5000, 9999, N // 2 + 3, N - 129, N - 1])
     for (b, h) in heads:
         q, k, v, do = (kept[(b, h, n)] for n in ("q", "k", "v", "do"))
         o_r, lse_r = O.forward_rows(q, k, v, rows, grid=grid)
