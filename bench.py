@@ -222,7 +222,7 @@ def graphed(fn):
 
 
 def timed(fn, iters, flush, warmup=3):
-    """Sum of per-iteration CUDA-event times (L2 flushed between iterations, outside the events)."""
+    """Per-iteration CUDA-event times in ms (L2 flushed between iterations, outside the events)."""
     import torch
 
     for _ in range(warmup):
@@ -235,7 +235,7 @@ def timed(fn, iters, flush, warmup=3):
         fn()
         b.record()
     torch.cuda.synchronize()
-    return sum(a.elapsed_time(b) for a, b in evs)
+    return [a.elapsed_time(b) for a, b in evs]
 
 
 def ncu_traffic(workload: str):
@@ -448,13 +448,18 @@ def run_ours(args, env):
             try:
                 sq, sk, sv, sdo, sspec = make_inputs(ws, device)
                 st = Step(sq, sk, sv, sdo, sspec)
-                it = 5
-                fms = timed(st.fwd if args.no_graph else graphed(st.fwd), it, flush) / it
+                it = args.sweep_iters
+                ft = timed(st.fwd if args.no_graph else graphed(st.fwd), it, flush)
                 st.fwd()
-                bms = timed(st.bwd if args.no_graph else graphed(st.bwd), it, flush) / it
+                bt = timed(st.bwd if args.no_graph else graphed(st.bwd), it, flush)
+                fms, bms = statistics.median(ft), statistics.median(bt)
                 ff, fb = flops(ws)
-                sweep.append({"workload": name, "desc": ws["desc"], "fwd_ms": round(fms, 4), "bwd_ms": round(bms, 4),
-                              "fwd_tflops": round(ff / fms / 1e9, 1), "bwd_tflops": round(fb / bms / 1e9, 1),
+                tf = lambda f, ms: round(f / ms / 1e9, 1)
+                sweep.append({"workload": name, "desc": ws["desc"], "calls": it,
+                              "fwd_ms": round(fms, 4), "bwd_ms": round(bms, 4),
+                              "fwd_tflops": tf(ff, fms), "bwd_tflops": tf(fb, bms),
+                              "fwd_tflops_min_max": [tf(ff, max(ft)), tf(ff, min(ft))],
+                              "bwd_tflops_min_max": [tf(fb, max(bt)), tf(fb, min(bt))],
                               "fwd_bwd_tflops": round((ff + fb) / (fms + bms) / 1e9, 1),
                               "fwd_frac": round(ff / fms / 1e9 / peaks["tflops"], 4),
                               "bwd_frac": round(fb / bms / 1e9 / peaks["tflops"], 4)})
@@ -463,8 +468,9 @@ def run_ours(args, env):
             except Exception as e:  # report, keep the headline
                 sweep.append({"workload": name, "error": repr(e)})
         out["sweep"] = sweep
-        out["sweep_note"] = ("per-call CUDA-event times (fwd = K1; bwd = K2+K3+K4, each call a CUDA graph replay unless "
-                             "--no-graph), L2 flushed between calls; frac vs measured burst peak")
+        out["sweep_note"] = ("median over `calls` per-call CUDA-event times (fwd = K1; bwd = K2+K3+K4, each call a CUDA "
+                             "graph replay unless --no-graph), L2 flushed between calls; *_min_max = TFLOP/s of the "
+                             "slowest and fastest call; frac vs measured burst peak")
     if clocks:
         out["clocks"] = clocks.stop()
     if env.rank == 0 and env.world == 1 and not args.no_cpu_baseline:
@@ -554,6 +560,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step's kernels eagerly (no CUDA graph)")
+    ap.add_argument("--sweep-iters", type=int, default=20, help="timed calls per sweep config (median reported)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
