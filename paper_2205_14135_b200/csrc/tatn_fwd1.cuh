@@ -313,10 +313,16 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
       for (;;) {
         Pos nx = cur;
         const bool has_next = advance(nx);
-        // QK of the next tile is issued before PV(cur) (it runs under softmax(cur)) unless it
-        // belongs to an item two or more items ahead: that item's Q reuses cur's Q buffer, which
-        // is reloaded only after cur's epilogue, i.e. after PV(cur).
-        const bool early = has_next && nx.n <= cur.n + 1;
+        // QK of the next tile is issued before PV(cur) (it runs under softmax(cur)) when both
+        // belong to the same item. At an item boundary PV(cur) goes first: the softmax warpgroup
+        // needs it for the epilogue (O) before it needs S(next), and QK(next) may still wait for the
+        // next item's Q / K to land — issued first it held PV(cur), and so the epilogue, behind those
+        // loads (traced: ~1.6K clk per boundary). An item two or more ahead reuses cur's Q buffer,
+        // which is reloaded only after cur's epilogue, so it must follow PV(cur) anyway.
+#ifndef TATN_FWD1_QK_BEFORE_LAST_PV
+#define TATN_FWD1_QK_BEFORE_LAST_PV 0  // 1: round-1 order (next item's first QK before the last PV)
+#endif
+        const bool early = has_next && (TATN_FWD1_QK_BEFORE_LAST_PV ? nx.n <= cur.n + 1 : nx.n == cur.n);
         if (early) {
           mbar_wait(BAR(kBarSFree), static_cast<uint32_t>(g & 1));  // S(g) is in registers
           issue_qk(nx, g + 1);

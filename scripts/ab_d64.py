@@ -17,8 +17,8 @@ for name in os.environ.get("AB_WORKLOADS", "gpt2-small,bert-large,long-8k-d64,bu
     q, k, v, do, spec = bench.make_inputs(w, torch.device("cuda"))
     st = bench.Step(q, k, v, do, spec)
     f = bench.flops(w)
-    fw = bench.timed(bench.graphed(st.fwd), 20, flush) / 20
-    bw = bench.timed(bench.graphed(st.bwd), 20, flush) / 20
+    fw = sorted(bench.timed(bench.graphed(st.fwd), 21, flush))[10]  # median
+    bw = sorted(bench.timed(bench.graphed(st.bwd), 21, flush))[10]
     res[name] = (round(f[0] / fw / 1e9), round(f[1] / bw / 1e9))
     del q, k, v, do, st
     torch.cuda.empty_cache()
