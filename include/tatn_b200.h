@@ -108,6 +108,14 @@ typedef struct {
    * the dropout hash. 0 for ordinary calls; else a multiple of 128 with k_offset + Nk <= Nq and
    * no block grid. Partial (o, lse) pairs of the shards combine with tatn_merge_partials. */
   int32_t k_offset;
+  /* Deterministic dQ (ABI v4): 0 = dQ partials of the key tiles are added into one fp32
+   * accumulator with atomic reductions (fastest; the summation order, and so the last bits of
+   * dQ, vary run to run); 1 = each key tile stores its partial in its own workspace slot and K4
+   * sums them in key-tile order, so dQ is bit-reproducible and an all-true block grid gives
+   * exactly the dense dQ (flash.hpp:62-63). The backward workspace grows by
+   * ceil(Nk/128) x B x H x Nq_pad x d x 4 bytes (practical for N <= 8K). O, LSE, dK, dV are
+   * deterministic in both modes. */
+  int32_t deterministic;
 } tatn_attn_desc;
 
 /* Merge R partial attention results over disjoint key shards (merge_stats, softmax.hpp:48-59,

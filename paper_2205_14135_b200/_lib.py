@@ -83,6 +83,7 @@ class TatnAttnDesc(ctypes.Structure):
         ("custom_words", ctypes.c_int32),
         ("custom_bstride", ctypes.c_int64),
         ("k_offset", ctypes.c_int32),
+        ("deterministic", ctypes.c_int32),
     ]
 
 

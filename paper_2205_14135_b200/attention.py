@@ -67,6 +67,9 @@ class AttnSpec:
     p_drop: float = 0.0  # dropout probability in [0, 1) (reference's positional PRNG, dropout.cpp)
     seed: int = 0  # dropout seed; slice (b, h) uses seed + b*H + h
     k_offset: int = 0  # key shard: key j is global key k_offset + j (sequence parallel; multiple of 128)
+    # dQ summed over key tiles in a fixed order (bit-reproducible; all-true grid == dense exactly);
+    # the backward workspace grows by ceil(Nk/128) x the dQ accumulator
+    deterministic: bool = False
     # mask="custom": bit-packed keep matrix from pack_custom_mask(), int32 [Nq, words] shared
     # by every slice or [B, Nq, words] per batch element (MaskSpec::custom_additive)
     custom: Optional[torch.Tensor] = None
@@ -236,6 +239,7 @@ def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttn
     desc.p_drop = float(spec.p_drop)
     desc.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
     desc.k_offset = int(spec.k_offset)
+    desc.deterministic = 1 if spec.deterministic else 0
     if spec.mask == "custom":
         cm = spec.custom
         if (cm is None or cm.dtype != torch.int32 or cm.dim() not in (2, 3) or not cm.is_contiguous()

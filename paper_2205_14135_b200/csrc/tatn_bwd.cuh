@@ -280,6 +280,57 @@ __global__ void __launch_bounds__(256) tatn_bwd_post(const float* __restrict__ d
   }
 }
 
+// ---------------------------------------------------------------- K4, deterministic dQ
+// dQ = sum over the key tiles j that visited the row's Q tile, in ascending j, of the partials K3
+// stored in slot j (plain stores, no atomics): bit-reproducible, and the same for a dense call and
+// an all-true block grid. Which (j, Q tile) pairs K3 visited is recomputed from K3's schedule
+// (make_bwd_sched; qt = K3's Q-tile height: 64, or the tf32 kernel's): causal ->
+// qt-tile index >= (128 j + k_off) / qt; key padding -> 128 j < valid_len[b] - k_off; block grid
+// -> grid[row / 128][j].
+template <int D, bool BF16, bool OUT_F32>
+__global__ void __launch_bounds__(256) tatn_bwd_post_det(const float* __restrict__ dq_part, void* __restrict__ dq,
+                                                         int64_t qb, int64_t qh, int64_t qn, int B, int H, int Nq,
+                                                         int Nq_pad, int tc, int qt, int causal, int k_off,
+                                                         const int32_t* __restrict__ valid_len,
+                                                         const uint8_t* __restrict__ grid) {
+  griddep_wait();  // programmatic dependent launch: inputs of the previous kernel visible
+  griddep_launch();
+  constexpr int kChunks = D / 8;
+  constexpr int kRowsPerBlock = 256 / kChunks;
+  const int c = static_cast<int>(threadIdx.x) % kChunks;
+  const int qi = static_cast<int>(blockIdx.x) * kRowsPerBlock + static_cast<int>(threadIdx.x) / kChunks;
+  const int h = static_cast<int>(blockIdx.y), b = static_cast<int>(blockIdx.z);
+  if (qi >= Nq) return;
+  const long long bh = static_cast<long long>(b) * H + h;
+  const long long slot = static_cast<long long>(B) * H * Nq_pad * D;
+  int kv_limit = 1 << 30;
+  if (valid_len != nullptr) kv_limit = valid_len[b] - k_off;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int j = 0; j < tc; ++j) {
+    bool visited;
+    if (grid != nullptr) visited = grid[static_cast<size_t>(qi / 128) * tc + j] != 0;
+    else visited = (!causal || qi / qt >= (128 * j + k_off) / qt) && 128 * j < kv_limit;
+    if (!visited) continue;
+    const float4* src = reinterpret_cast<const float4*>(dq_part + j * slot + (bh * Nq_pad + qi) * D + c * 8);
+    const float4 x = src[0], y = src[1];
+    a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+    a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+  }
+  const size_t off = static_cast<size_t>(b) * qb + static_cast<size_t>(h) * qh + static_cast<size_t>(qi) * qn + c * 8;
+  if constexpr (OUT_F32) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(dq) + off);
+    dst[0] = make_float4(a[0], a[1], a[2], a[3]);
+    dst[1] = make_float4(a[4], a[5], a[6], a[7]);
+  } else {
+    uint4 out;
+    out.x = pack2<BF16>(a[0], a[1]);
+    out.y = pack2<BF16>(a[2], a[3]);
+    out.z = pack2<BF16>(a[4], a[5]);
+    out.w = pack2<BF16>(a[6], a[7]);
+    *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dq) + off) = out;
+  }
+}
+
 // ---------------------------------------------------------------- K2b (Custom masks only)
 // Transpose the keep bits [nb][Nq][words] (query rows) into [nb][Nk][Nq_pad/32] (key rows), so
 // K3's softmax thread (one key row) reads its 64 query bits of a Q tile with one 8-byte load.
@@ -843,9 +894,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // accumulator: lanes hold consecutive head-dim columns, so each instruction is one
         // coalesced 64-byte reduction, and no shared-memory bandwidth is spent on dQ
         if (active) {
-          float* dst = p.dq_acc + (static_cast<size_t>(it.bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D + dd;
+          if (p.dq_part != nullptr) {  // deterministic: this key tile's own slot, plain stores (K4 sums in j order)
+            float* dst = p.dq_part + ((static_cast<size_t>(it.j) * p.B * p.H + it.bh) * Nq_pad +
+                                      static_cast<size_t>(i) * kBwdQT) * D + dd;
 #pragma unroll
-          for (int c = 0; c < 64; ++c) atomicAdd(dst + c * D, __uint_as_float(v[c]) * tau);
+            for (int c = 0; c < 64; ++c) dst[c * D] = __uint_as_float(v[c]) * tau;
+          } else {
+            float* dst = p.dq_acc + (static_cast<size_t>(it.bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D + dd;
+#pragma unroll
+            for (int c = 0; c < 64; ++c) atomicAdd(dst + c * D, __uint_as_float(v[c]) * tau);
+          }
         }
         continue;
         }
@@ -860,10 +918,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         named_bar_sync(2, 128);
         if (leader) {
-          float* dst = p.dq_acc + (static_cast<size_t>(it.bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D;
-          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
-                       "r"(sDQ), "r"(Cfg::kDQBytes)
-                       : "memory");
+          if (p.dq_part != nullptr) {  // deterministic: bulk store into this key tile's own slot
+            float* dst = p.dq_part + ((static_cast<size_t>(it.j) * p.B * p.H + it.bh) * Nq_pad +
+                                      static_cast<size_t>(i) * kBwdQT) * D;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sDQ),
+                         "r"(Cfg::kDQBytes)
+                         : "memory");
+          } else {
+            float* dst = p.dq_acc + (static_cast<size_t>(it.bh) * Nq_pad + static_cast<size_t>(i) * kBwdQT) * D;
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                         "r"(sDQ), "r"(Cfg::kDQBytes)
+                         : "memory");
+          }
           bulk_commit();
           TATN_EV(g, 6);
           if (g == 2) TATN_TRACE_AT(13);
@@ -973,6 +1039,25 @@ int sm_count();
 cudaError_t ensure_smem_attr(const void* kern, int bytes);
 bool make_map_4d_ext(CUtensorMap* map, int dtype, const void* base, int d, int n, int H, int B, const int64_t str[3],
                      int box_rows, bool mn_major = false);
+// deterministic dQ: the per-key-tile partial slots, the last region of the backward workspace
+inline float* dq_part_ptr(const tatn_attn_desc& d, void* ws) {
+  const size_t rows = static_cast<size_t>(d.B) * d.H * ((d.Nq + 127) / 128 * 128);
+  size_t off = rows * d.d * sizeof(float) + 2 * rows * sizeof(float) + 16;
+  if (d.mask_kind == TATN_MASK_CUSTOM) {
+    const size_t nb = d.custom_bstride != 0 ? static_cast<size_t>(d.B) : 1;
+    off += nb * static_cast<size_t>(d.Nk) * ((d.Nq + 127) / 128 * 4) * sizeof(uint32_t);
+  }
+  return reinterpret_cast<float*>(static_cast<char*>(ws) + off);
+}
+template <int D, bool BF16, bool OUT_F32>
+cudaError_t launch_post_det(const tatn_attn_desc& d, const float* dq_part, void* dq, int Nq_pad, int qt,
+                            cudaStream_t stream) {
+  const dim3 blocks(static_cast<unsigned>((d.Nq + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
+  return launch(tatn_dev::tatn_bwd_post_det<D, BF16, OUT_F32>, blocks, dim3(256), 0, stream, dq_part, dq, d.q_str[0],
+                d.q_str[1], d.q_str[2], d.B, d.H, d.Nq, Nq_pad, (d.Nk + 127) / 128, qt,
+                d.mask_kind == TATN_MASK_CAUSAL ? 1 : 0, d.k_offset,
+                d.mask_kind == TATN_MASK_KEY_PADDING ? d.valid_len : nullptr, d.block_grid);
+}
 }
 
 template <int D, bool BF16, bool OUT_F32, bool DROP>
@@ -989,6 +1074,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   uint32_t* custom_t = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(item_counter) + 16);
   const int custom_t_words = Nq_pad / 32;
   const bool custom = d.mask_kind == TATN_MASK_CUSTOM;
+  float* dq_part = d.deterministic ? tatn_host::dq_part_ptr(d, ws) : nullptr;
   if (custom) {
     const int nb = d.custom_bstride != 0 ? d.B : 1;
     const long long warps = static_cast<long long>(nb) * custom_t_words * ((d.Nk + 31) / 32);
@@ -1033,6 +1119,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   p.n_items = d.B * d.H * p.n_ktiles;
   p.item_counter = item_counter;
   p.custom_t = custom ? custom_t : nullptr;
+  p.dq_part = dq_part;
   p.custom_t_words = custom_t_words;
   p.custom_t_b = (custom && d.custom_bstride != 0) ? 1 : 0;
   p.k_off = d.k_offset;
@@ -1067,9 +1154,12 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
   if (e != cudaSuccess) return e;
   {
     const dim3 blocks(static_cast<unsigned>((d.Nq + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
-    e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, BF16, OUT_F32>, blocks, dim3(256), 0, stream,
-                          static_cast<const float*>(dq_acc), dq, d.q_str[0], d.q_str[1], d.q_str[2], d.B, d.H, d.Nq,
-                          Nq_pad);
+    if (dq_part != nullptr)
+      e = tatn_host::launch_post_det<D, BF16, OUT_F32>(d, dq_part, dq, Nq_pad, tatn_dev::kBwdQT, stream);
+    else
+      e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, BF16, OUT_F32>, blocks, dim3(256), 0, stream,
+                            static_cast<const float*>(dq_acc), dq, d.q_str[0], d.q_str[1], d.q_str[2], d.B, d.H, d.Nq,
+                            Nq_pad);
     if (e != cudaSuccess) return e;
   }
   *launches = custom ? 4 : 3;

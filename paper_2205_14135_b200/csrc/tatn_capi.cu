@@ -151,6 +151,7 @@ int validate(const tatn_attn_desc* d) {
   if (d->k_offset != 0 && d->block_grid != nullptr) return TATN_E_UNSUPPORTED;
   if (d->Nq > (1 << 24) || static_cast<int64_t>(d->B) * d->H * ((d->Nq + 127) / 128) > (1ll << 31) - 1)
     return TATN_E_SHAPE;
+  if (d->deterministic != 0 && d->deterministic != 1) return TATN_E_ARG;
   return TATN_OK;
 }
 
@@ -264,6 +265,7 @@ cudaError_t launch_bwd_tf32(const tatn_attn_desc& d, const void* q, const void* 
   p.custom = d.mask_kind == TATN_MASK_CUSTOM ? d.custom_mask : nullptr;
   p.custom_words = d.custom_words;
   p.custom_bstride = d.custom_bstride;
+  p.dq_part = d.deterministic ? tatn_host::dq_part_ptr(d, ws) : nullptr;
   set_dropout(d, &p.drop_seed, &p.drop_thresh, &p.drop_scale);
   auto kern = tatn_dev::tatn_bwd_tf32_kernel<D, DROP>;
   e = tatn_host::ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
@@ -275,9 +277,12 @@ cudaError_t launch_bwd_tf32(const tatn_attn_desc& d, const void* q, const void* 
   if (prof_stop) cudaEventRecord(prof_stop, stream);
   if (e != cudaSuccess) return e;
   const dim3 qblocks(static_cast<unsigned>((d.Nq + 256 / (D / 8) - 1) / (256 / (D / 8))), d.H, d.B);
-  e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, false, true>, qblocks, dim3(256), 0, stream,
-                        static_cast<const float*>(dq_acc), dq, d.q_str[0], d.q_str[1], d.q_str[2], d.B, d.H, d.Nq,
-                        Nq_pad);
+  if (p.dq_part != nullptr)
+    e = tatn_host::launch_post_det<D, false, true>(d, p.dq_part, dq, Nq_pad, Cfg::QT, stream);
+  else
+    e = tatn_host::launch(tatn_dev::tatn_bwd_post<D, false, true>, qblocks, dim3(256), 0, stream,
+                          static_cast<const float*>(dq_acc), dq, d.q_str[0], d.q_str[1], d.q_str[2], d.B, d.H, d.Nq,
+                          Nq_pad);
   if (e != cudaSuccess) return e;
   *launches = 3;
   return cudaSuccess;
@@ -518,6 +523,8 @@ size_t tatn_bwd_workspace_bytes(const tatn_attn_desc* desc) {
     const size_t nb = desc->custom_bstride != 0 ? static_cast<size_t>(desc->B) : 1;
     bytes += nb * static_cast<size_t>(desc->Nk) * ((desc->Nq + 127) / 128 * 4) * sizeof(uint32_t);
   }
+  if (desc->deterministic)  // + per-key-tile dQ partials [tc][B*H][Nq_pad][d]
+    bytes += static_cast<size_t>((desc->Nk + 127) / 128) * rows * desc->d * sizeof(float);
   return bytes;
 }
 

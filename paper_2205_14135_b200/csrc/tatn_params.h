@@ -58,6 +58,7 @@ struct BwdParams {
   int custom_t_words;        // Nq_pad / 32
   int custom_t_b;            // 1: one mask per batch element (b), 0: shared
   int k_off;                 // global index of key 0 (sequence-parallel key shards; multiple of 128)
+  float* dq_part;            // deterministic dQ: per-key-tile partials [tc][B*H][Nq_pad][d] (else nullptr)
   const uint32_t* custom;    // Custom mask as given (tf32 check mode reads it untransposed)
   int custom_words;
   int64_t custom_bstride;

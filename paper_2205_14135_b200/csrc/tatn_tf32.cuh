@@ -543,17 +543,28 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     }
     mbar_wait(kBarB, ph);
     tc_fence_after();
-    // dQ partial (tau applied) -> fp32 workspace accumulator
+    // dQ partial (tau applied) -> the fp32 workspace accumulator (red.global.add), or in the
+    // deterministic mode this key tile's own slot (plain stores; K4 sums the slots in j order)
     const uint32_t tDQ = tmem_base + lane_off + Cfg::kTmemDQ;
-    float* acc = p.dq_acc + static_cast<size_t>(bh) * Nq_pad * D;
+    const bool det = p.dq_part != nullptr;
+    float* acc = det ? p.dq_part + (static_cast<size_t>(j) * p.B * p.H + bh) * Nq_pad * D
+                     : p.dq_acc + static_cast<size_t>(bh) * Nq_pad * D;
     if constexpr (D == 64) {  // thread = query row i0 + r, columns = d
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tDQ + 32 * c, v);
         float* dst = acc + static_cast<size_t>(i0 + r) * D + 32 * c;
+        if (det) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) atomicAdd(dst + e, __uint_as_float(v[e]) * p.tau);
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(dst + e) =
+                make_float4(__uint_as_float(v[e]) * p.tau, __uint_as_float(v[e + 1]) * p.tau,
+                            __uint_as_float(v[e + 2]) * p.tau, __uint_as_float(v[e + 3]) * p.tau);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) atomicAdd(dst + e, __uint_as_float(v[e]) * p.tau);
+        }
       }
     } else {  // thread = head-dim index r, columns = queries
 #pragma unroll
@@ -561,8 +572,11 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
         uint32_t v[32];
         tmem_ld32(tDQ + 32 * c, v);
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          atomicAdd(acc + static_cast<size_t>(i0 + 32 * c + e) * D + r, __uint_as_float(v[e]) * p.tau);
+        for (int e = 0; e < 32; ++e) {
+          float* dst = acc + static_cast<size_t>(i0 + 32 * c + e) * D + r;
+          if (det) *dst = __uint_as_float(v[e]) * p.tau;
+          else atomicAdd(dst, __uint_as_float(v[e]) * p.tau);
+        }
       }
     }
     tc_fence_before();

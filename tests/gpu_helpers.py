@@ -43,11 +43,12 @@ def empty_like_layout(t: torch.Tensor, dtype=None) -> torch.Tensor:
 
 
 def run_gpu(q, k, v, do, dtype, mask="none", valid_len=None, grid=None, backward=True, layout="bhnd",
-            visited=False, out_fp32=False, p_drop=0.0, seed=0, custom=None, block_size=(128, 128)):
+            visited=False, out_fp32=False, p_drop=0.0, seed=0, custom=None, block_size=(128, 128),
+            deterministic=False):
     """Forward (+ backward) on the device through the C ABI. Returns numpy fp64 outputs.
     custom: bool keep matrix [Nq, Nk] (shared) or [B, Nq, Nk] for mask="custom"."""
     qd, kd, vd = (to_dev(t, dtype, layout) for t in (q, k, v))
-    spec = A.AttnSpec(mask=mask, out_fp32=out_fp32, p_drop=p_drop, seed=seed)
+    spec = A.AttnSpec(mask=mask, out_fp32=out_fp32, p_drop=p_drop, seed=seed, deterministic=deterministic)
     if custom is not None:
         spec.custom = A.pack_custom_mask(torch.from_numpy(np.asarray(custom, dtype=bool)).cuda())
     if valid_len is not None:

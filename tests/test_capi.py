@@ -141,6 +141,16 @@ def test_workspace_formula():
     assert lib.tatn_bwd_workspace_bytes(ctypes.byref(good_desc(B=0))) == 0
 
 
+def test_deterministic_workspace_and_flag():
+    lib = _lib.load()
+    d = good_desc()
+    base = lib.tatn_bwd_workspace_bytes(ctypes.byref(d))
+    d.deterministic = 1
+    rows = 2 * 3 * 384
+    assert lib.tatn_bwd_workspace_bytes(ctypes.byref(d)) == base + 3 * rows * 64 * 4  # tc = 3 key tiles
+    assert validate(good_desc(deterministic=2)) == _lib.TATN_E_ARG
+
+
 def test_custom_mask_descriptor():
     buf = (ctypes.c_uint32 * (300 * 12 + 4))()
     base = (ctypes.addressof(buf) + 15) // 16 * 16
