@@ -22,6 +22,7 @@
 #include "tatn/random.hpp"
 #include "tatn/reference.hpp"
 #include "tatn/tile_plan.hpp"
+#include "flash_b200_multi.hpp"
 
 namespace tatn::b200 {
 void set_input_dtype_fp16(bool fp16);
@@ -284,6 +285,49 @@ int main() {
         FlashSaved dense = flash_forward(q, k, v, cfg, plan, m1);
         FlashSaved sp = blocksparse_forward(q, k, v, cfg, plan, all, m2);
         report("bs_alltrue_br64_bit_identical_forward", dense.o == sp.o && dense.stats.m == sp.stats.m);
+      }
+    }
+
+    // ---- the reference's concurrency model over devices: heads split across workers (one host thread
+    // per worker, worker w on device w % ndev), private MemoryModels merged with AccessCounter::merge;
+    // identical outputs to the per-head calls, merged counters == their sum (peak = max)
+    {
+      const size_t n = 384, d = 64;
+      const TilePlan plan = plan_tiles(n, d, 116224);
+      std::vector<Matrix> qs, ks, vs, dos;
+      for (int h = 0; h < 7; ++h) {
+        qs.push_back(rounded(gaussian_matrix(n, d, 300 + 4 * h)));
+        ks.push_back(rounded(gaussian_matrix(n, d, 301 + 4 * h)));
+        vs.push_back(rounded(gaussian_matrix(n, d, 302 + 4 * h)));
+        dos.push_back(rounded(gaussian_matrix(n, d, 303 + 4 * h)));
+      }
+      std::vector<b200::HeadProblem> heads;
+      std::vector<const Matrix*> dop;
+      for (int h = 0; h < 7; ++h) {
+        AttnConfig cfg = AttnConfig::make(n, d);
+        cfg.mask = (h & 1) ? MaskSpec::causal() : MaskSpec::none();
+        heads.push_back({&qs[h], &ks[h], &vs[h], cfg});
+        dop.push_back(&dos[h]);
+      }
+      MemoryModel one(plan.m_capacity);
+      std::vector<FlashSaved> seq;
+      std::vector<Gradients> seqg;
+      for (int h = 0; h < 7; ++h) seq.push_back(flash_forward(qs[h], ks[h], vs[h], heads[h].cfg, plan, one));
+      for (int h = 0; h < 7; ++h) seqg.push_back(flash_backward(seq[h], qs[h], ks[h], vs[h], dos[h], one));
+      for (int workers : {0, 3}) {
+        MemoryModel merged(plan.m_capacity);
+        auto sh = b200::flash_forward_sharded(heads, plan, merged, workers);
+        auto shg = b200::flash_backward_sharded(sh, heads, dop, merged, workers);
+        bool same = sh.size() == 7 && shg.size() == 7;
+        for (int h = 0; same && h < 7; ++h)
+          same = sh[h].o == seq[h].o && sh[h].stats.m == seq[h].stats.m && shg[h].dq == seqg[h].dq &&
+                 shg[h].dk == seqg[h].dk && shg[h].dv == seqg[h].dv;
+        report("sharded_workers" + std::to_string(workers) + "_outputs_equal_per_head_calls", same);
+        report("sharded_workers" + std::to_string(workers) + "_counters_merged",
+               merged.counter().hbm_read_elems == one.counter().hbm_read_elems &&
+                   merged.counter().hbm_write_elems == one.counter().hbm_write_elems &&
+                   merged.counter().flops == one.counter().flops &&
+                   merged.counter().peak_resident_elems == one.counter().peak_resident_elems);
       }
     }
 

@@ -23,6 +23,8 @@ REQUIRED = [
     "tatn::flop_model(", "tatn::byte_report(", "tatn::BlockMask::count_true()",
     # the reference's own sources linked in (oracle side of the acceptance run)
     "tatn::standard_forward(", "tatn::standard_backward(", "tatn::memeff_forward(",
+    # the reference's concurrency model over the box's GPUs (flash_b200_multi.hpp)
+    "tatn::b200::flash_forward_sharded(", "tatn::b200::flash_backward_sharded(",
 ]
 
 
