@@ -22,10 +22,12 @@
 #include "tatn/random.hpp"
 #include "tatn/reference.hpp"
 #include "tatn/tile_plan.hpp"
+#include "tatn_b200.h"
 #include "flash_b200_multi.hpp"
 
 namespace tatn::b200 {
 void set_input_dtype_fp16(bool fp16);
+void set_input_dtype(int dtype);
 }
 
 using namespace tatn;
@@ -429,6 +431,33 @@ int main() {
       report(tag + "_forward", close(s.o, r.o), fmt(max_abs(s.o, r.o), rel_l2(s.o, r.o)));
       report(tag + "_backward", close(g.dq, rg.dq) && close(g.dk, rg.dk) && close(g.dv, rg.dv),
              fmt(max_abs(g.dv, rg.dv), rel_l2(g.dv, rg.dv)));
+    }
+
+    // ---- fp32 input mode (tf32 check mode; BASELINE configs[0]: N = 512, d = 64, non-causal, fp32): the
+    // reference's fp64 engines on the same fp32 inputs, at the fp32 bar (max abs 2e-3, rel-L2 1e-3)
+    {
+      b200::set_input_dtype(TATN_DTYPE_FP32);
+      const size_t n = 512, d = 64;
+      for (int causal = 0; causal < 2; ++causal) {
+        AttnConfig cfg = AttnConfig::make(n, d);
+        if (causal) cfg.mask = MaskSpec::causal();
+        Matrix q = gaussian_matrix(n, d, 41), k = gaussian_matrix(n, d, 42), v = gaussian_matrix(n, d, 43),
+               dO = gaussian_matrix(n, d, 44);
+        for (Matrix* m : {&q, &k, &v, &dO})
+          for (double& x : m->data()) x = static_cast<double>(static_cast<float>(x));  // the fp32 inputs
+        const TilePlan plan = plan_tiles(n, d, 65536);
+        MemoryModel mem(plan.m_capacity);
+        FlashSaved s = flash_forward(q, k, v, cfg, plan, mem);
+        Gradients g = flash_backward(s, q, k, v, dO, mem);
+        ForwardArtifacts r = standard_forward(q, k, v, cfg);
+        Gradients rg = standard_backward(r, q, k, v, dO, cfg);
+        const std::string tag = causal ? "fp32_inputs_c1_causal" : "fp32_inputs_c1";
+        report(tag + "_forward", close(s.o, r.o, 2e-3, 1e-3), fmt(max_abs(s.o, r.o), rel_l2(s.o, r.o)));
+        report(tag + "_backward",
+               close(g.dq, rg.dq, 2e-3, 1e-3) && close(g.dk, rg.dk, 2e-3, 1e-3) && close(g.dv, rg.dv, 2e-3, 1e-3),
+               fmt(max_abs(g.dq, rg.dq), rel_l2(g.dq, rg.dq)));
+      }
+      b200::set_input_dtype(TATN_DTYPE_BF16);
     }
 
     // ---- fp16 input mode
