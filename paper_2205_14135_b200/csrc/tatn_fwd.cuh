@@ -24,7 +24,10 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy O rescale (log2 units)
 // exp2 pairs per group of 8 computed by the polynomial on the FMA pipe instead of MUFU
 // (MUFU.EX2 retires 16/clk/SM). Swept on B200 (r01): 1 of 8 is best (+3-5%); 2 or 3 of 8
 // lose to the extra FMA-pipe issue. Full tiles only (masked tiles hold -inf).
-constexpr int kEmuPairs = 1;
+#ifndef TATN_EMU_PAIRS
+#define TATN_EMU_PAIRS 1
+#endif
+constexpr int kEmuPairs = TATN_EMU_PAIRS;
 // d = 128 keeps every exp2 on MUFU: there the MMA and MUFU are balanced and the FMA-pipe
 // polynomial measured slower (N = 8K causal fwd 889 -> 912 TFLOP/s without it)
 template <int D>
