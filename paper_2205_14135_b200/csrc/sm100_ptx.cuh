@@ -484,6 +484,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // TATN_EV_INIT caches the trace pointer in a register (a global load per event would
 // perturb the timeline it measures)
 #define TATN_EV_INIT() unsigned long long* const tatn_ev_buf = (blockIdx.x == 0) ? g_tatn_trace : nullptr
+// per-item events of CTA 0 (item n < 256, slot ev < 4) after the per-tile region
+#define TATN_EVI(n, ev)                                                                                  \
+  do {                                                                                                   \
+    if (tatn_ev_buf && (n) < 256)                                                                        \
+      tatn_ev_buf[200000ull * 16 + 8192 + static_cast<unsigned long long>(n) * 4 + (ev)] = clock64();    \
+  } while (0)
 #define TATN_EV(g, ev)                                                                                   \
   do {                                                                                                   \
     if (tatn_ev_buf && (g) < 1024)                                                                       \
@@ -495,6 +501,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #define TATN_EV(g, ev) \
   do {                 \
+  } while (0)
+#define TATN_EVI(n, ev) \
+  do {                  \
   } while (0)
 #endif
 

@@ -533,9 +533,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       __syncwarp();
       if (w < 0) break;
+      if (lane == 0) TATN_EVI(n, 0);  // claimed and published
       const Item it = item(w, n);
       const int kb = n % NKV;
       if (n >= NKV) mbar_wait(BAR(kBarKVFree + kb), static_cast<uint32_t>((n / NKV - 1) & 1));
+      if (lane == 0) TATN_EVI(n, 1);  // K / V buffer free: load issued next
       if (elect_one_sync()) {
         const uint32_t sK = sKV + kb * 2 * Cfg::kKVTile, sV = sK + Cfg::kKVTile;
         mbar_expect_tx(BAR(kBarKVFull + kb), 2 * Cfg::kKVTile);
@@ -594,7 +596,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int kb = n % NKV;
       const uint32_t koff = static_cast<uint32_t>(kb * 2 * Cfg::kKVTile);  // K of buffer kb
       const uint32_t voff = koff + Cfg::kKVTile;
+      if (lane == 0) TATN_EVI(n, 2);  // MMA warp starts the item (item taken)
       mbar_wait(BAR(kBarKVFull + kb), static_cast<uint32_t>((n / NKV) & 1));
+      if (lane == 0) TATN_EVI(n, 3);  // K / V landed
       tc_fence_after();
       if (lane == 0 && n == 0) TATN_TRACE_AT(1);
 #ifdef TATN_TRACE

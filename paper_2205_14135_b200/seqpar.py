@@ -4,9 +4,13 @@ extension, PAPER.md:1718-1726).
 One long sequence, R ranks (one process per GPU). Rank r holds every query and the key /
 value shard [k0_r, k1_r) (tile-aligned, ``shard_range``). Forward: each rank runs the sm_100a
 forward on its shard with ``k_offset = k0_r`` (global key indices for causal / padding /
-custom masks and the dropout hash) and fp32 partial outputs; the one exchange step is an
-all-gather of the partial (O_r, LSE_r); ``tatn_merge_partials`` combines them with the
-reference's merge_stats algebra (softmax.hpp:48-59, softmax.cpp:62-83). Backward: each rank
+custom masks and the dropout hash) and fp32 partial outputs. The exchange is an all-gather of
+the partial LSE_r only (R x B x H x Nq floats) and an all-reduce (sum) of fp32 O-sized shares:
+with LSE_rest = logsumexp of the other ranks' LSE, ``tatn_merge_partials`` over the pair
+(O_r, LSE_r), (0, LSE_rest) — the reference's merge_stats algebra (softmax.hpp:48-59,
+softmax.cpp:62-83) — gives rank r's share O_r exp(LSE_r - LSE) and the global LSE, and the shares
+sum to O. Memory and traffic stay at one O per rank (an all-gather of the partial O would move R
+of them). Backward: each rank
 runs the backward on its shard against the merged (O, LSE) — D = rowsum(dO * O) and P are
 then global — which yields the shard's dK, dV exactly and a partial dQ over the shard's keys;
 the exchange is an all-reduce (sum) of the fp32 partial dQ.
@@ -44,11 +48,11 @@ class KeyShardedAttention:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
 
     # ------------------------------------------------------------------ compute steps
-    def _partial_fwd(self, q, k, v, spec):
+    def _partial_fwd(self, q, k, v, spec, out=None):
         from . import attention as A
 
         spec = dataclasses.replace(spec, out_fp32=True)
-        o = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+        o = torch.empty(q.shape, dtype=torch.float32, device=q.device) if out is None else out
         return A.flash_fwd(q, k, v, spec, out=o)
 
     def _merge(self, o_parts, lse_parts, out_dtype):
@@ -76,13 +80,20 @@ class KeyShardedAttention:
         if k_local.shape[2] != k1 - k0:
             raise ValueError(f"rank {self.rank}: key shard has {k_local.shape[2]} rows, expected {k1 - k0}")
         local = dataclasses.replace(spec, k_offset=k0)
+        # [2, B, H, Nq, d] fp32: slot 0 = this shard's partial O_r, slot 1 = zeros (the "rest" partial)
+        pair = torch.zeros((2,) + tuple(q.shape), dtype=torch.float32, device=q.device)
         if k1 > k0:
-            o_p, lse_p = self._partial_fwd(q, k_local, v_local, local)
+            _, lse_p = self._partial_fwd(q, k_local, v_local, local, out=pair[0])
         else:  # an empty shard contributes nothing (LSE = -inf)
-            o_p = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
             lse_p = torch.full(q.shape[:3], float("-inf"), dtype=torch.float32, device=q.device)
-        o_parts, lse_parts = self._all_gather(o_p), self._all_gather(lse_p)
-        o32, lse = self._merge(o_parts, lse_parts, torch.float32)
+        lse_all = self._all_gather(lse_p)  # the only gather: R x B x H x Nq floats
+        others = torch.cat([lse_all[:self.rank], lse_all[self.rank + 1:]])
+        lse_rest = (torch.logsumexp(others, dim=0) if others.shape[0] else
+                    torch.full_like(lse_p, float("-inf")))
+        # this rank's share O_r exp(LSE_r - LSE) and the global LSE, then the sum over ranks
+        o32, lse = self._merge(pair, torch.stack([lse_p, lse_rest]).contiguous(), torch.float32)
+        if self.world > 1:
+            dist.all_reduce(o32, op=dist.ReduceOp.SUM, group=self.group)
         return o32.to(q.dtype), lse, o32
 
     def backward(self, q, k_local, v_local, o32, do, lse, spec, n_keys: int):

@@ -12,17 +12,22 @@ for (B, H, N, d, mask) in [(8, 12, 1024, 64, "causal"), (1, 32, 4096, 128, "caus
     spec = A.AttnSpec(mask=mask)
     o, lse = A.flash_fwd(q, k, v, spec)
     for _ in range(3): A.flash_bwd(q, k, v, o, do, lse, spec)
-    buf = torch.zeros(200000 * 16 + 1024 * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(200000 * 16 + 1024 * 8 + 1024, dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
     lib.tatn_debug_set_trace(ctypes.c_void_p(buf.data_ptr()))
     torch.cuda.synchronize()
     A.flash_bwd(q, k, v, o, do, lse, spec); torch.cuda.synchronize()
     lib.tatn_debug_set_trace(ctypes.c_void_p(0))
-    ev = buf[200000 * 16:].view(1024, 8).cpu().numpy().astype(np.int64)
+    evi = buf[200000 * 16 + 8192:200000 * 16 + 8192 + 1024].view(256, 4).cpu().numpy().astype(np.int64)
+    ev = buf[200000 * 16:200000 * 16 + 8192].view(1024, 8).cpu().numpy().astype(np.int64)
     n = int((ev[:, 1] > 0).sum())
     ev = ev[:n]
     t0 = ev[ev > 0].min()
     print(f"== B{B} H{H} N{N} d{d} {mask}: CTA0 tiles {n}, span {(ev.max() - t0)} cyc, per tile {(ev[:,1].max()-ev[:,0].min())/max(n-1,1):.0f} cyc")
+    ni = int((evi[:, 0] > 0).sum())
+    print("   items (claimed / KV-free / MMA took item / KV landed):")
+    for n_ in range(ni):
+        print(f"   item {n_}: " + " ".join(f"{(x - t0) if x > 0 else -1:9d}" for x in evi[n_]))
     print("   g  " + " ".join(f"{x:>9}" for x in names))
     for g in range(min(n, 40)):
         print(f"  {g:3d} " + " ".join(f"{(x - t0) if x > 0 else -1:9d}" for x in ev[g]))

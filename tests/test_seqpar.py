@@ -2,9 +2,9 @@
 
 CPU: the shard partition; the merge algebra (numpy restatement of tatn_merge_partials /
 merge_stats, softmax.cpp:62-83) recombines per-shard oracle results into full attention;
-a 2- and 3-rank gloo run of KeyShardedAttention's orchestration (all-gather of partials,
-all-reduce of dQ) with the oracle standing in for the kernels reproduces single-process
-attention. GPU: the kernels with k_offset on R virtual shards + tatn_merge_partials against
+a 2- and 3-rank gloo run of KeyShardedAttention's orchestration (all-gather of the partial
+LSEs, pairwise merge into this rank's share of O, all-reduce of the shares and of dQ) with the
+oracle standing in for the kernels reproduces single-process attention. GPU: the kernels with k_offset on R virtual shards + tatn_merge_partials against
 the oracle (north-star tolerance) for causal / none / key padding / custom / dropout, and the
 merge kernel against its restatement.
 """
@@ -84,9 +84,13 @@ class _OracleSharded(KeyShardedAttention):
     def _keep(self, q, spec, nk):
         return _shard_keep(q.shape[2], spec.k_offset, spec.k_offset + nk, self.kind)
 
-    def _partial_fwd(self, q, k, v, spec):
+    def _partial_fwd(self, q, k, v, spec, out=None):
         o, lse = O.forward(q.numpy(), k.numpy(), v.numpy(), mask="custom", custom=self._keep(q, spec, k.shape[2]))
-        return torch.from_numpy(o).float(), torch.from_numpy(lse).float()
+        o = torch.from_numpy(o).float()
+        if out is not None:
+            out.copy_(o)
+            o = out
+        return o, torch.from_numpy(lse).float()
 
     def _merge(self, o_parts, lse_parts, out_dtype):
         o, lse = merge_np(o_parts.double().numpy(), lse_parts.double().numpy())
@@ -208,3 +212,39 @@ def test_gpu_merge_kernel_empty_rows_and_dtypes(cuda_device):
         np.testing.assert_allclose(o.double().cpu().numpy(), mo, atol=tol, rtol=tol)
         np.testing.assert_allclose(lse.double().cpu().numpy(), ml, atol=2e-5)
         assert torch.all(o[:, :, 5] == 0) and torch.all(torch.isneginf(lse[:, :, 5]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R,mask", [(2, "causal"), (3, "none"), (4, "causal")])
+def test_gpu_pairwise_shares_sum_to_full_attention(cuda_device, R, mask):
+    """The forward exchange KeyShardedAttention uses: each shard's fp32 partial merged with
+    (0, logsumexp of the other shards' LSE) by tatn_merge_partials is O_r exp(LSE_r - LSE); the
+    shares sum (the all-reduce) to full attention, and every pair yields the global LSE."""
+    from paper_2205_14135_b200 import attention as A
+    from tests import gpu_helpers as G
+
+    B, H, N, d = 2, 2, 700, 64
+    q, k, v, do = G.make_inputs(B, H, N, N, d, "bf16")
+    ref = G.oracle_full(q, k, v, do, mask=mask, backward=False)
+    qd, kd, vd = (G.to_dev(t, "bf16") for t in (q, k, v))
+
+    class Virtual(KeyShardedAttention):
+        def __init__(self, r):
+            self.group, self.world, self.rank = None, R, r
+
+    parts = []
+    for r in range(R):
+        sp = Virtual(r)
+        k0, k1 = sp.local_keys(N)
+        local = A.AttnSpec(mask=mask, k_offset=k0)
+        pair = torch.zeros((2,) + tuple(qd.shape), dtype=torch.float32, device="cuda")
+        _, lse_r = sp._partial_fwd(qd, kd[:, :, k0:k1].contiguous(), vd[:, :, k0:k1].contiguous(), local, out=pair[0])
+        parts.append((pair, lse_r))
+    lse_all = torch.stack([p[1] for p in parts])
+    total = torch.zeros(qd.shape, dtype=torch.float32, device="cuda")
+    for r, (pair, lse_r) in enumerate(parts):
+        others = torch.cat([lse_all[:r], lse_all[r + 1:]])
+        share, lse = A.merge_partials(pair, torch.stack([lse_r, torch.logsumexp(others, 0)]).contiguous())
+        total += share
+        G.assert_close("lse", lse.double().cpu().numpy(), ref["lse"])
+    G.assert_close("o", total.double().cpu().numpy(), ref["o"])
