@@ -330,6 +330,33 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- block-grid bitmasks
+// Bitmask of the nonzero entries of a u8 vector (entry i at base[i * stride], i < n) into
+// dst[0 .. ceil(n / 32)), by one whole warp. The loads of 16 ballot rounds are issued before the
+// ballots, so the (L2-latency-bound, possibly strided) reads of a long grid row / column overlap
+// instead of costing one round trip per 32 entries (N = 64K: 16 rounds per item).
+#ifndef TATN_MASK_ROUNDS
+#define TATN_MASK_ROUNDS 4  // A/B (butterfly N = 64K bwd): 1 -> 493, 4 -> 542, 8 -> 545, 16 -> 514 TFLOP/s; 16K equal
+#endif
+template <typename Store>
+__device__ __forceinline__ void warp_nonzero_bits(const uint8_t* base, int n, int64_t stride, uint32_t lane,
+                                                  Store store) {
+  constexpr int R = TATN_MASK_ROUNDS;  // ballot rounds whose loads are in flight together
+  for (int b0 = 0; b0 < n; b0 += 32 * R) {
+    uint32_t v[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = b0 + 32 * u + static_cast<int>(lane);
+      v[u] = (base != nullptr && i < n) ? __ldg(base + static_cast<int64_t>(i) * stride) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, v[u] != 0u);
+      if (lane == 0 && b0 + 32 * u < n) store((b0 >> 5) + u, bits);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- dropout
 // splitmix64 finaliser of the reference's positional generator (dropout.cpp:7-12).
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {

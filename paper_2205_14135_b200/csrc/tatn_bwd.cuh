@@ -462,16 +462,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   auto build_col_mask = [&](int w, uint32_t* dst) {  // whole producer warp
     int bh0, j0;
     bwd_item(p, w, bh0, j0);
-    const uint8_t* gcol = p.grid + j0;
-    for (int base = 0; base < p.tr; base += 32) {
-      const int r = base + lane;
-      const bool v = r < p.tr && gcol[static_cast<size_t>(r) * p.tc] != 0;
-      const uint32_t bits = __ballot_sync(0xffffffffu, v);
-      if (lane == 0) {
-        dst[(2 * base) >> 5] = spread_bits16(bits);
-        dst[((2 * base) >> 5) + 1] = spread_bits16(bits >> 16);
-      }
-    }
+    // strided column of the grid: 128-row blocks -> bits over 64-row Q tiles (each bit doubled)
+    warp_nonzero_bits(p.grid + j0, p.tr, p.tc, lane_id(), [&](int wd, uint32_t bits) {
+      dst[2 * wd] = spread_bits16(bits);
+      dst[2 * wd + 1] = spread_bits16(bits >> 16);
+    });
     __syncwarp();
   };
   constexpr bool kSparsePersistent = Cfg::kMaskSlots == kItemRing;

@@ -183,11 +183,7 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
         fwd1_item(p, w, bh0, qt0);
         const uint8_t* grow_ptr = qt0 < p.tr ? p.grid + static_cast<size_t>(qt0) * p.tc : nullptr;
         uint32_t* slot_mask = mask_smem + (n % Cfg::kRing) * 64;
-        for (int base = 0; base < p.tc; base += 32) {
-          const int t = base + lane;
-          const uint32_t bits = __ballot_sync(0xffffffffu, grow_ptr != nullptr && t < p.tc && grow_ptr[t] != 0);
-          if (lane == 0) slot_mask[base >> 5] = bits;
-        }
+        warp_nonzero_bits(grow_ptr, p.tc, 1, lane, [&](int wd, uint32_t bits) { slot_mask[wd] = bits; });
         __syncwarp();
       }
       if (lane == 0) {

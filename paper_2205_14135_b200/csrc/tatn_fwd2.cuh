@@ -193,11 +193,7 @@ __global__ void __launch_bounds__(384, 1)
           const int qt = pair0 * 2 + q;
           const uint8_t* row = qt < p.tr ? p.grid + static_cast<size_t>(qt) * p.tc : nullptr;
           uint32_t* dst = mask_smem + ((n % Cfg::kRing) * 2 + q) * 64;
-          for (int base = 0; base < p.tc; base += 32) {
-            const int t = base + lane;
-            const uint32_t bits = __ballot_sync(0xffffffffu, row != nullptr && t < p.tc && row[t] != 0);
-            if (lane == 0) dst[base >> 5] = bits;
-          }
+          warp_nonzero_bits(row, p.tc, 1, static_cast<uint32_t>(lane), [&](int wd, uint32_t bits) { dst[wd] = bits; });
         }
         __syncwarp();
       }
