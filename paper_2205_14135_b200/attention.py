@@ -181,23 +181,32 @@ def lower_block_mask(spec: "AttnSpec", B: int, Nq: int, Nk: int) -> "AttnSpec":
     return replace(spec, block_grid=tiles, block_size=(128, 128), mask="custom", custom=bits, valid_len=None)
 
 
-def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttnDesc:
-    """Pack a tatn_attn_desc, checking every shape / dtype / device the ABI cannot see (a
-    descriptor that disagrees with the buffers would let the kernels read or write out of
-    bounds)."""
-    for name, t in (("q", q), ("k", k), ("v", v)) + ((("o", o),) if check_o else ()):
+def check_shapes(q, k, v, o=None):
+    """The buffer shapes a descriptor is built from must agree: q [B, H, Nq, d], k and v
+    [B, H, Nk, d], o (if given) like q. The ABI sees only the descriptor, so a mismatch here would
+    let the kernels read or write past a buffer."""
+    for name, t in (("q", q), ("k", k), ("v", v)) + ((("o", o),) if o is not None else ()):
         if t.dim() != 4:
             raise ValueError(f"{name} must be [B, H, N, d], got shape {tuple(t.shape)}")
-        if t.device != q.device or t.device.type != "cuda":
-            raise ValueError(f"{name} must be a CUDA tensor on {q.device}, got {t.device}")
     B, H, Nq, d = q.shape
     Nk = k.shape[2]
     if tuple(k.shape) != (B, H, Nk, d):
         raise ValueError(f"k shape {tuple(k.shape)} does not match q {tuple(q.shape)} (expected [B, H, Nk, d])")
     if tuple(v.shape) != tuple(k.shape):
         raise ValueError(f"v shape {tuple(v.shape)} != k shape {tuple(k.shape)}")
-    if check_o and tuple(o.shape) != tuple(q.shape):
+    if o is not None and tuple(o.shape) != tuple(q.shape):
         raise ValueError(f"o shape {tuple(o.shape)} != q shape {tuple(q.shape)}")
+    return B, H, Nq, Nk, d
+
+
+def make_desc(q, k, v, o, spec: AttnSpec, check_o: bool = True) -> _lib.TatnAttnDesc:
+    """Pack a tatn_attn_desc, checking every shape / dtype / device the ABI cannot see (a
+    descriptor that disagrees with the buffers would let the kernels read or write out of
+    bounds)."""
+    B, H, Nq, Nk, d = check_shapes(q, k, v, o if check_o else None)
+    for name, t in (("q", q), ("k", k), ("v", v)) + ((("o", o),) if check_o else ()):
+        if t.device != q.device or t.device.type != "cuda":
+            raise ValueError(f"{name} must be a CUDA tensor on {q.device}, got {t.device}")
     spec = lower_block_mask(spec, B, Nq, Nk)
     desc = _lib.TatnAttnDesc()
     desc.B, desc.H, desc.Nq, desc.Nk, desc.d = B, H, Nq, Nk, d
