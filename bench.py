@@ -39,6 +39,8 @@ UNIT = "TFLOP/s"
 
 # BASELINE.json configs. The headline (N=1) is configs[1]; the others are sweep lines.
 WORKLOADS = {
+    "c1-fp32": dict(B=2, H=4, N=512, d=64, dtype="fp32", mask="none",
+                    desc="C1 B=2 H=4 N=512 d=64 non-causal fp32 inputs (BASELINE configs[0], tf32 check mode)"),
     "gpt2-small": dict(B=8, H=12, N=1024, d=64, dtype="fp16", mask="causal",
                        desc="GPT-2 small attention B=8 H=12 N=1024 d=64 causal fp16 (BASELINE configs[1])"),
     "bert-large": dict(B=16, H=16, N=512, d=64, dtype="bf16", mask="key_padding",
@@ -57,7 +59,7 @@ WORKLOADS = {
     "butterfly-64k": dict(B=1, H=16, N=65536, d=64, dtype="bf16", mask="none", grid="butterfly",
                           desc="configs[4] block-sparse butterfly N=64K d=64"),
 }
-SWEEP = ["bert-large", "long-2k", "long-4k", "long-8k", "long-16k", "long-4k-noncausal", "long-8k-d64",
+SWEEP = ["c1-fp32", "bert-large", "long-2k", "long-4k", "long-8k", "long-16k", "long-4k-noncausal", "long-8k-d64",
          "butterfly-16k", "butterfly-64k"]
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
@@ -162,7 +164,7 @@ def make_inputs(w, device, seed=0, shard=None):
 
     from paper_2205_14135_b200 import attention as A
 
-    dt = torch.bfloat16 if w["dtype"] == "bf16" else torch.float16
+    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[w["dtype"]]
     g = torch.Generator(device=device).manual_seed(seed)
     shape = (w["B"], w["H"], w["N"], w["d"]) if shard is None else (shard.n_local, 1, w["N"], w["d"])
     q, k, v, do = (torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(dt) for _ in range(4))
