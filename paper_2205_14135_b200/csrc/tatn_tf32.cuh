@@ -124,6 +124,10 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     tatn_fwd_tf32_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, const FwdParams p) {
   using Cfg = Tf32FwdCfg<D>;
+#ifdef TATN_TRACE  // per-step stamps of CTA (0, 0, 0) (trace builds only)
+  unsigned long long* const tatn_ev_buf = (blockIdx.x | blockIdx.y | blockIdx.z) == 0 ? g_tatn_trace : nullptr;
+  if (threadIdx.x == 0) TATN_EV(0, 7);
+#endif
   extern __shared__ uint8_t smem_raw[];
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
@@ -147,6 +151,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     tmem_relinquish();
   }
   griddep_wait();
+  if (threadIdx.x == 0) TATN_EV(0, 5);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -192,6 +197,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     }
   }
   mbar_wait(kBarQ, 0);
+  if (threadIdx.x == 0) TATN_EV(0, 6);
   tf32_round_smem(sQ, Cfg::kTile);
   constexpr uint32_t idesc_qk = make_idesc_f16(kFmtTf32, 128, 128, 0, 0);
   constexpr uint32_t idesc_pv = make_idesc_f16(kFmtTf32, 128, D, 0, 1);
@@ -200,6 +206,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     const int tn = next_tile(t + 1);
     const uint32_t ph = static_cast<uint32_t>(n & 1);
     mbar_wait(kBarK, ph);
+    if (threadIdx.x == 0) TATN_EV(n, 1);
     tf32_round_smem(sK, Cfg::kTile);
     fence_proxy_async_smem();  // the rounded tiles are read by the tensor core (async proxy)
     named_bar_sync(1, kTf32Threads);
@@ -216,6 +223,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
       }
     }
     mbar_wait(kBarS, ph);
+    if (threadIdx.x == 0) TATN_EV(n, 2);
     tc_fence_after();
     if (leader && tn < T) {  // K buffer free (the QK MMA completed): prefetch the next K tile
       mbar_expect_tx(kBarK, Cfg::kTile);
@@ -230,21 +238,33 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
                                              static_cast<size_t>(qi) * p.custom_words + (p.k_off + k0) / 32);
     }
     const uint32_t cwa[4] = {cw.x, cw.y, cw.z, cw.w};
+    // Only tiles that reach past the key limit, cross the causal diagonal or carry a Custom mask
+    // need the per-element predicate (uniform over the CTA: it depends on the tile, not the row).
+    const bool need_mask = (k0 + 128 > kv_limit) || (causal && p.k_off + k0 + 127 > q0) || custom_on;
     // scaled score of column 32 c + i (log2 domain), -inf where masked
     auto score = [&](int c, int i, uint32_t raw) {
       const int kj = k0 + 32 * c + i;
       const bool masked = kj >= kv_limit || (causal && p.k_off + kj > qi) || ((cwa[c] >> i) & 1u) == 0u;
       return masked ? -INFINITY : __uint_as_float(raw) * sl2;
     };
-    // pass 1: row max over the tile (S stays in TMEM; pass 2 reads it again)
-    float mx = -INFINITY;
+    // pass 1: row max over the tile (S stays in TMEM; pass 2 reads it again). Four independent
+    // partial maxima / sums: with one warp per SM sub-partition a single 128-long dependency chain
+    // (fmax, then add) was the softmax's critical path (traced: ~15K cycles per tile)
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t v[32];
       tmem_ld32(tS + 32 * c, v);
+      if (need_mask) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, score(c, i, v[i]));
+        for (int i = 0; i < 32; ++i) m4[i & 3] = fmaxf(m4[i & 3], score(c, i, v[i]));
+      } else {  // sl2 > 0: scale the maximum once
+#pragma unroll
+        for (int i = 0; i < 32; ++i) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(v[i]));
+      }
     }
+    float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    if (!need_mask) mx *= sl2;
     const float m_new = fmaxf(m_run, mx);
     const bool grow = m_new > m_run;
     const float alpha = grow ? ex2_approx(m_run - m_new) : 1.f;  // 0 when m_run == -inf
@@ -264,26 +284,30 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     }
     const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
     // pass 2: P = 2^(s - m) rounded to tf32, written over S (the A operand of P V)
+    float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t v[32];
       tmem_ld32(tS + 32 * c, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const float pv = round_tf32(ex2_approx(score(c, i, v[i]) - m_use));
-        l_run += pv;
+        const float x = need_mask ? score(c, i, v[i]) - m_use : fmaf(__uint_as_float(v[i]), sl2, -m_use);
+        const float pv = round_tf32(ex2_approx(x));
+        l4[i & 3] += pv;
         float pm = pv;
         if constexpr (DROP) pm = drop_keep(drow, p.k_off + k0 + 32 * c + i, p.drop_thresh) ? round_tf32(pv * p.drop_scale) : 0.f;
         v[i] = __float_as_uint(pm);
       }
       tmem_st32(tS + 32 * c, v);
     }
+    l_run += (l4[0] + l4[1]) + (l4[2] + l4[3]);
     mbar_wait(kBarV, ph);
     tf32_round_smem(sV, Cfg::kTile);
     fence_proxy_async_smem();
     tmem_st_wait();
     tc_fence_before();
     named_bar_sync(1, kTf32Threads);
+    if (threadIdx.x == 0) TATN_EV(n, 3);
     if (leader) {
       tc_fence_after();
 #pragma unroll
@@ -293,6 +317,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
       mma_commit(kBarO);
     }
     mbar_wait(kBarO, ph);
+    if (threadIdx.x == 0) TATN_EV(n, 4);
     tc_fence_after();
     if (leader && tn < T) {  // V buffer free: prefetch the next V tile
       mbar_expect_tx(kBarV, Cfg::kTile);
