@@ -509,6 +509,9 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     tf32_reswizzle<D, QT>(sQ);
     tf32_reswizzle<D, QT>(sDO);
     named_bar_sync(1, kTf32Threads);  // row vectors staged, re-swizzle done
+    // only tiles that reach past the key limit, cross the causal diagonal or carry a Custom mask
+    // evaluate the per-element predicate (uniform over the CTA for this Q tile)
+    const bool need_mask = (k0 + 128 > kv_limit) || (causal && p.k_off + k0 + 127 > i0) || custom_on;
 #pragma unroll 1
     for (int cc = 0; cc < QT / 32; ++cc) {
       uint32_t sv[32], dv[32];
@@ -521,9 +524,11 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
         const int qi = i0 + c;
         const int kg = p.k_off + kj;
         float pv = ex2_approx(fmaf(__uint_as_float(sv[e]), sl2, vec[c]));
-        const bool masked = kj >= kv_limit || (causal && kg > qi) ||
-                            (custom_on && (qi >= p.Nq || !custom_keep(p.custom, p.custom_words, p.custom_bstride, b, qi, kg)));
-        pv = masked ? 0.f : pv;
+        if (need_mask) {  // rows past Nq need no predicate: their -lse2 = -inf gives P = 0
+          const bool masked = kj >= kv_limit || (causal && kg > qi) ||
+                              (custom_on && (qi >= p.Nq || !custom_keep(p.custom, p.custom_words, p.custom_bstride, b, qi, kg)));
+          pv = masked ? 0.f : pv;
+        }
         const float dpv = __uint_as_float(dv[e]);
         if constexpr (DROP) {  // dP through the mask, dV from P * Z / (1 - p) (reference.cpp:118-141)
           const float z = drop_keep(drows[c], kg, p.drop_thresh) ? p.drop_scale : 0.f;
