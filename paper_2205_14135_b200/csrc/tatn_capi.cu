@@ -34,6 +34,10 @@ using tatn_host::schedule_group;
 namespace {
 
 thread_local int g_last_launches = 0;
+
+// every tensor base pointer must be 16-byte aligned: TMA tiles and the kernels' 16-byte vector
+// loads / stores (rows are 16-byte multiples by the stride rule) assume it
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 // forward workspace: the persistent kernels' self-resetting item counter {next item, finished
 // CTAs}; zero before first use, left zero by every completed launch
 constexpr size_t kFwdWorkspaceBytes = 16;
@@ -431,6 +435,7 @@ int tatn_fwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   int st = validate(desc);
   if (st != TATN_OK) return st;
   if (!q || !k || !v || !o || !lse || !workspace) return TATN_E_ARG;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return TATN_E_ARG;
   if (workspace_bytes < kFwdWorkspaceBytes) return TATN_E_WORKSPACE;
   if ((reinterpret_cast<uintptr_t>(workspace) & 15u) != 0) return TATN_E_ARG;
   const tatn_attn_desc& d = *desc;
@@ -534,6 +539,9 @@ int tatn_bwd(const tatn_attn_desc* desc, const void* q, const void* k, const voi
   int st = validate(desc);
   if (st != TATN_OK) return st;
   if (!q || !k || !v || !o || !dO || !lse || !dq || !dk || !dv || !workspace) return TATN_E_ARG;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(dO) || !aligned16(dq) ||
+      !aligned16(dk) || !aligned16(dv) || !aligned16(workspace))
+    return TATN_E_ARG;
   if (workspace_bytes < tatn_bwd_workspace_bytes(desc)) return TATN_E_WORKSPACE;
   if (desc->dtype == TATN_DTYPE_FP32) {
     const int sel = (desc->d == 128 ? 2 : 0) + (desc->p_drop > 0.0 ? 1 : 0);

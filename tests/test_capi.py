@@ -89,6 +89,12 @@ def test_forward_workspace():
     assert st == _lib.TATN_E_WORKSPACE
     st = lib.tatn_fwd(ctypes.byref(d), one, one, one, one, one, base + 4, 16, None)
     assert st == _lib.TATN_E_ARG
+    # tensor base pointers must be 16-byte aligned (TMA tiles, 16-byte vector accesses)
+    odd = ctypes.c_void_p(base + 2)
+    st = lib.tatn_fwd(ctypes.byref(d), one, odd, one, one, one, base, 16, None)
+    assert st == _lib.TATN_E_ARG
+    st = lib.tatn_bwd(ctypes.byref(d), one, one, odd, one, one, one, one, one, one, base, 1 << 30, None)
+    assert st == _lib.TATN_E_ARG
 
 
 @pytest.mark.parametrize(
