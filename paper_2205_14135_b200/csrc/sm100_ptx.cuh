@@ -84,10 +84,29 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 // Watchdog: a wait that has not completed after ~2^35 SM cycles (~17 s at 1.965 GHz)
 // is a deadlock; trap so the launch fails loudly instead of hanging the device.
 constexpr long long kWatchdogCycles = 1ll << 35;
+#ifdef TATN_WAIT_DEBUG
+// debug builds: a wait stuck for ~1 s records (block, thread, barrier, parity) in g_tatn_wait_dbg
+// (host-mapped, so it survives the watchdog trap) and keeps waiting
+__device__ unsigned long long* g_tatn_wait_dbg = nullptr;
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+#ifdef TATN_WAIT_DEBUG
+    if (clock64() - t0 > (1ll << 31) && g_tatn_wait_dbg) {  // record once, keep waiting (host-mapped buffer)
+      const unsigned long long i = atomicAdd(g_tatn_wait_dbg, 1ull);
+      if (i < 1000)
+        g_tatn_wait_dbg[1 + i] = (static_cast<unsigned long long>(blockIdx.x) << 40) |
+                                 (static_cast<unsigned long long>(threadIdx.x) << 28) |
+                                 (static_cast<unsigned long long>(bar & 0xffffu) << 4) | parity;
+      __threadfence_system();
+      while (!mbar_try_wait(bar, parity)) {
+        if (clock64() - t0 > kWatchdogCycles) __trap();
+      }
+      return;
+    }
+#endif
     if (clock64() - t0 > kWatchdogCycles) __trap();
   }
 }
@@ -522,12 +541,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (tatn_ev_buf && (g) < 1024)                                                                       \
       tatn_ev_buf[200000ull * 16 + static_cast<unsigned long long>(g) * 8 + (ev)] = clock64();           \
   } while (0)
+// a second bank of 8 per-tile events (after the per-item region)
+#define TATN_EV2(g, ev)                                                                                  \
+  do {                                                                                                   \
+    if (tatn_ev_buf && (g) < 1024)                                                                       \
+      tatn_ev_buf[200000ull * 16 + 9216 + static_cast<unsigned long long>(g) * 8 + (ev)] = clock64();    \
+  } while (0)
 #else
 #define TATN_EV_INIT() \
   do {                 \
   } while (0)
 #define TATN_EV(g, ev) \
   do {                 \
+  } while (0)
+#define TATN_EV2(g, ev) \
+  do {                  \
   } while (0)
 #define TATN_EVI(n, ev) \
   do {                  \

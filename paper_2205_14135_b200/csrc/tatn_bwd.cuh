@@ -12,12 +12,13 @@
 //   K3 tatn_bwd_kernel: per (b, h, key tile) loop over 64-row Q tiles
 //   K4 tatn_bwd_post  : dQ = bf16/fp16(dQacc)
 //
-// K3 CTA layout (448 threads):
+// K3 CTA layout (d = 64: 480 threads, d = 128: 448):
 //   warps 0-3 "softmax 0": thread = key row (TMEM lane). Recompute P^T, dS^T for even Q tiles.
 //   warps 4-7 "softmax 1": the same for odd Q tiles (ping-pong: two tiles in softmax at once).
 //   warps 8-11 "dQ":       thread = head-dim row of dQ^T (TMEM lane); stage + bulk reduce.
 //   warp 12   TMA producer (K, V once; Q_i, dO_i, lse2_i, D_i ring)
-//   warp 13   TMEM allocator + tcgen05.mma issuer
+//   warp 13   TMEM allocator + tcgen05.mma issuer (d = 64: the fronts)
+//   warp 14   d = 64 only: tcgen05.mma issuer of the backs (dV, dK, dQ^T)
 // Per Q tile i the MMA computes (M = 128 keys unless noted)
 //   front: S^T = K Q_i^T, dP^T = V dO_i^T                      (N = 64 queries)
 //   back : dV += P^T dO_i, dK += dS^T Q_i  (A from TMEM)       (N = d)
@@ -41,7 +42,7 @@
 #define TATN_BWD_SEP_STAGE 1  // d = 64: dK / dV staging in its own shared-memory region
 #endif
 #ifndef TATN_BWD_STAGES_D64
-#define TATN_BWD_STAGES_D64 4  // d = 64 Q / dO ring depth
+#define TATN_BWD_STAGES_D64 5  // d = 64 Q / dO ring depth (the early front (g + 2) reads stage (g + 2) % S)
 #endif
 #ifndef TATN_BWD_DS_BUFS
 #define TATN_BWD_DS_BUFS 2  // d = 64 dS^T buffers (3 measured no faster: the softmax is not waiting on them)
@@ -52,7 +53,6 @@
 
 namespace tatn_dev {
 
-constexpr int kBwdThreads = 448;
 constexpr int kBwdQT = 64;    // query rows per Q tile
 constexpr int kBwdKT = 128;   // keys per CTA
 
@@ -69,7 +69,8 @@ struct BwdCfg {
   // g waits for the dQ^T MMA of tile g - 3, not g - 2 (issued after the front of tile g)
   static constexpr int kDSBufs = (D == 64) ? TATN_BWD_DS_BUFS : 2;
   static_assert(kDSBufs >= 2, "the ping-pong needs two dS^T buffers");
-  static constexpr int kDQBytes = kBwdQT * D * 4;     // fp32 staging
+  // fp32 dQ staging (d = 64 issues its dQ reductions from registers: no staging)
+  static constexpr int kDQBytes = (TATN_DQ_RED && D == 64) ? 0 : kBwdQT * D * 4;
   static constexpr int kVecBytes = 2 * kBwdQT * 4;    // lse2 + D
   // K/V buffers: double-buffered at d = 64 (the next item's K/V lands while this one runs)
   static constexpr int kKVBufs = (D == 64) ? 2 : 1;
@@ -95,12 +96,17 @@ struct BwdCfg {
   static_assert(kSmemBytes <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
   static_assert(2 * 128 * D * 2 <= kOffVec - kOffDS, "dK/dV staging must fit the dS^T + dQ staging region");
   static constexpr uint32_t kTmemX = 0;    // X_x = x*128: S^T [0,64) dP^T [64,128)
-  static constexpr uint32_t kTmemDV = 256;
-  static constexpr uint32_t kTmemDK = 256 + D;
-  // d = 64 leaves 128 TMEM columns free: dQ^T gets its own two buffers there, so the next
-  // front (S^T into X_x) need not wait for the dQ warpgroup to drain dQ^T out of X_x.
-  static constexpr bool kSepDQ = (D == 64);
-  static constexpr uint32_t kTmemDQ = 384;  // [384 + 64x, 448 + 64x) when kSepDQ
+  // d = 64: P^T / dS^T (16-bit) go to their own columns PdS_x = [256 + 64x, 320 + 64x) (P^T
+  // [0,32), dS^T [32,64)) instead of over S^T / dP^T, so the softmax releases X_x as soon as it
+  // holds S^T / dP^T in registers and the front of Q tile g + 2 runs under the rest of its work
+  // (with X_x aliased the front had to wait for back(g)); dQ^T(g) then lands in PdS_x once
+  // back(g) has read P^T / dS^T. d = 128 has no free columns: P^T / dS^T alias X_x.
+  static constexpr bool kEarlyX = (D == 64);
+  // warps 0-7 softmax, 8-11 dQ, 12 TMA producer, 13 MMA (d = 64: fronts), 14 (d = 64) MMA backs
+  static constexpr int kThreads = kEarlyX ? 480 : 448;
+  static constexpr uint32_t kTmemPdS = 256;
+  static constexpr uint32_t kTmemDV = kEarlyX ? 384 : 256;
+  static constexpr uint32_t kTmemDK = kTmemDV + D;
   // dQ partials by red.global.add from registers (d = 64: frees the shared-memory port of
   // the staging write + bulk-reduce read); d = 128 keeps smem staging + one bulk reduce,
   // which measured faster there (r01 sweep)
@@ -378,7 +384,7 @@ __device__ __forceinline__ void bwd_item(const BwdParams& p, int w, int& bh, int
 constexpr int kItemRing = 4;  // items published by the producer warp to the other roles
 
 template <int D, bool BF16, bool OUT_F32, bool DROP>
-__global__ void __launch_bounds__(kBwdThreads, 1)
+__global__ void __launch_bounds__(BwdCfg<D, DROP>::kThreads, 1)
     tatn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
@@ -386,7 +392,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   using Cfg = BwdCfg<D, DROP>;
   constexpr int S = Cfg::kStages;
   constexpr int NKV = Cfg::kKVBufs;
-  constexpr int kProducerWarp = 12, kMmaWarp = 13;
+  constexpr int kProducerWarp = 12, kMmaWarp = 13, kBackWarp = 14;
+  constexpr int kConsumerWarps = Cfg::kThreads / 32 - 1;  // every warp but the producer reads the item ring
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // 128B-swizzle atoms need 1024B alignment
   const uint32_t smem_base = smem_u32(smem_raw);
@@ -409,7 +416,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int kBarPFull = kBarSFull + 2;      // [2]
   const int kBarDQFull = kBarPFull + 2;     // [2]
   const int kBarDQEmpty = kBarDQFull + 2;   // [2]
-  const int kBarDSEmpty = kBarDQEmpty + 2;  // [kDSBufs]
+  const int kBarXFree = kBarDQEmpty + 2;    // [2] d = 64: S^T / dP^T of X_x in registers (count 128)
+  const int kBarDSEmpty = kBarXFree + 2;    // [kDSBufs]
   const int kBarKVFull = kBarDSEmpty + Cfg::kDSBufs;  // [NKV]
   const int kBarKVFree = kBarKVFull + NKV;  // [NKV] MMAs of the buffer's item done
   const int kBarFinal = kBarKVFree + NKV;   // item's MMAs done (dK, dV final in TMEM)
@@ -418,9 +426,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // store has read (a softmax warpgroup may skip items, so it waits on a count, not a parity)
   const int kBarStageFree = kBarAccFree + 1;
   const int kBarItem = kBarStageFree + 1;   // [kItemRing] item id published
-  const int kBarItemFree = kBarItem + kItemRing;  // [kItemRing] slot read by all 13 consumer warps
+  const int kBarItemFree = kBarItem + kItemRing;  // [kItemRing] slot read by every consumer warp
   const int kNumBars = kBarItemFree + kItemRing;
-  static_assert(8 * (2 * S + 8 + Cfg::kDSBufs + 2 * NKV + 3 + 2 * kItemRing) <= 8 * 46, "barrier region");
+  static_assert(8 * (2 * S + 10 + Cfg::kDSBufs + 2 * NKV + 3 + 2 * kItemRing) <= 8 * 46, "barrier region");
   volatile int* ring = reinterpret_cast<volatile int*>(smem_gen + Cfg::kOffRing);
   // Dense launches are persistent (one CTA per SM): the producer claims items from a
   // global counter (zeroed by K2) and publishes them; block-sparse launches run exactly
@@ -449,9 +457,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int x = 0; x < 2; ++x) {
       mbar_init(BAR(kBarPFull + x), 128);
       mbar_init(BAR(kBarDQEmpty + x), 128);
+      mbar_init(BAR(kBarXFree + x), 128);
     }
     mbar_init(BAR(kBarAccFree), 128);
-    for (int k = 0; k < kItemRing; ++k) mbar_init(BAR(kBarItemFree + k), 13);
+    for (int k = 0; k < kItemRing; ++k) mbar_init(BAR(kBarItemFree + k), kConsumerWarps);
+    if (Cfg::kEarlyX)
+      for (int k = 0; k < NKV; ++k) mbar_init(BAR(kBarKVFree + k), 2);  // front and back issuers
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -567,9 +578,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer
-    // whole warp runs the schedule (waits); one elected lane issues tcgen05.mma/commit
+  } else if (!Cfg::kEarlyX && warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer, d = 128
+    // whole warp runs the schedule (waits); one elected lane issues tcgen05.mma/commit (d = 64
+    // runs the single-lane two-issuer schedule below)
     constexpr uint32_t ab = BF16 ? 1u : 0u;
     constexpr uint32_t idesc_s = make_idesc_f16(ab, 128, kBwdQT, 0, 0);   // S^T, dP^T
     constexpr uint32_t idesc_acc = make_idesc_f16(ab, 128, D, 0, 1);      // dV, dK (B MN-major)
@@ -638,8 +650,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int i = 0; i < cnt && i < 2; ++i) {
         const int g = g0 + i;
         front_dp(g, voff);
-        if (!Cfg::kSepDQ && g >= 2) wait_dq_drained(g - 2);  // X_x still holds dQ^T(g - 2)
+        if (g >= 2) wait_dq_drained(g - 2);  // X_x still holds dQ^T(g - 2)
         front_s(g, koff);
+      }
+      if (n > 0) {  // previous dK / dV drained (every item, empty ones included: see the d = 64 issuer)
+        mbar_wait(BAR(kBarAccFree), static_cast<uint32_t>((n - 1) & 1));
+        tc_fence_after();
       }
       for (int i = 0; i < cnt; ++i) {
         const int g = g0 + i;
@@ -648,10 +664,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(BAR(kBarPFull + x), static_cast<uint32_t>((g >> 1) & 1));
         tc_fence_after();
         if (lane == 0) TATN_EV(g, 2);
-        if (i == 0 && n > 0) {
-          mbar_wait(BAR(kBarAccFree), static_cast<uint32_t>((n - 1) & 1));  // previous dK / dV drained
-          tc_fence_after();
-        }
         if (lane == 0 && i == 2 && n == 0) TATN_TRACE_AT(11);
         const uint32_t accf = i > 0 ? 1u : 0u;
         if (elect_one_sync()) {
@@ -669,7 +681,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         auto issue_dq = [&]() {
           // dQ^T = K^T dS^T  (K MN-major as A; dS^T MN-major as B; 16 keys per step)
-          const uint32_t tDQ = tmem_base + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
+          const uint32_t tDQ = tmem_base + Cfg::kTmemX + x * 128;
           if (elect_one_sync()) {
 #pragma unroll
             for (int kk = 0; kk < kBwdKT / 16; ++kk)
@@ -682,22 +694,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
           if (lane == 0) TATN_EV(g, 4);
         };
-        if constexpr (Cfg::kSepDQ) {
-          // X_x is free once dV/dK have read P^T / dS^T (in-order pipe): start the next front
-          // first so S^T(g + 2) reaches the softmax warpgroup one dQ^T earlier
-          if (i + 2 < cnt) {
-            front_dp(g + 2, voff);
-            front_s(g + 2, koff);
-          }
-          if (g >= 2) wait_dq_drained(g - 2);  // dQ^T buffer x free
-          issue_dq();
-        } else {
-          issue_dq();  // dQ^T lands in X_x cols [0,64): the next front waits for the dQ warpgroup
-          if (i + 2 < cnt) {
-            front_dp(g + 2, voff);
-            wait_dq_drained(g);
-            front_s(g + 2, koff);
-          }
+        issue_dq();  // dQ^T lands in X_x cols [0,64): the next front waits for the dQ warpgroup
+        if (i + 2 < cnt) {
+          front_dp(g + 2, voff);
+          wait_dq_drained(g);
+          front_s(g + 2, koff);
         }
       }
       if (elect_one_sync()) {
@@ -708,6 +709,150 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       w_next = take_item(n + 1);
       g0 += cnt;
     }
+  } else if (Cfg::kEarlyX && (warp == kMmaWarp || warp == kBackWarp)) {
+    // ------------------------------------------------------------ MMA issuers
+    // One elected lane runs a whole schedule (waits, tcgen05.mma, commits). Inside a single
+    // elect region ptxas knows one lane is active and issues each MMA group straight from
+    // uniform registers; with the warp running the loop and electing a lane per group it
+    // wrapped every tcgen05.mma in an elect / vote loop (scripts/micro/mma_issue.cu: the d = 64
+    // Q-tile stream 1600-1800 -> 1050 cycles). At d = 64 the fronts (S^T, dP^T into X_x) and the
+    // backs (dV, dK, dQ^T: PdS_x, accumulators) touch disjoint TMEM, so two warps issue them:
+    // warp 13 the fronts, warp 14 the backs, and neither waits behind the other's barrier waits
+    // and descriptor set-up (the issuing lane, not the tensor pipe, set the pace with one warp).
+    // Each warp's tcgen05.commit tracks its own MMAs; the K/V buffer is free once both have
+    // committed (kBarKVFree counts 2).
+    constexpr uint32_t ab = BF16 ? 1u : 0u;
+    constexpr uint32_t idesc_s = make_idesc_f16(ab, 128, kBwdQT, 0, 0);   // S^T, dP^T
+    constexpr uint32_t idesc_acc = make_idesc_f16(ab, 128, D, 0, 1);      // dV, dK (B MN-major)
+    // dQ^T (A, B MN-major): M = d; at d = 64 an M = 64 MMA (half the A bytes of M = 128)
+    constexpr uint32_t idesc_dq = make_idesc_f16(ab, Cfg::kDQ64 ? 64 : 128, kBwdQT, 1, 1);
+    // base descriptors; per-MMA operands add (byte offset >> 4) to the start-address field
+    const uint64_t dKV0 = make_sdesc_sw128(sKV, 16, 1024);               // K / V as K-major A
+    const uint64_t dQk0 = make_sdesc_sw128(sQ, 16, 1024);                // Q as K-major B
+    const uint64_t dDOk0 = make_sdesc_sw128(sDO, 16, 1024);              // dO as K-major B
+    const uint64_t dQmn0 = make_sdesc_sw128(sQ, Cfg::kQSub, 1024);       // Q as MN-major B
+    const uint64_t dDOmn0 = make_sdesc_sw128(sDO, Cfg::kQSub, 1024);     // dO as MN-major B
+    const uint64_t dKmn0 = make_sdesc_sw128(sKV, 128 * 128, 1024);       // K^T as MN-major A
+    const uint64_t dDS0 = make_sdesc_sw128(sDS, 128 * 128, 1024);        // dS^T as MN-major B
+    const bool fronts = warp == kMmaWarp;                                // else the backs
+    if (elect_one_sync()) {
+      // take_item for a single lane: the ring slot's consumer arrival is this warp's one arrival
+      auto take_item_1 = [&](int n) -> int {
+        mbar_wait(BAR(kBarItem + n % kItemRing), static_cast<uint32_t>((n / kItemRing) & 1));
+        const int w = ring[n % kItemRing];
+        mbar_arrive(BAR(kBarItemFree + n % kItemRing));
+        return w;
+      };
+      auto front_dp = [&](int g, uint32_t voff) {  // dP^T = V dO^T  -> X cols [64,128)
+        const int s = g % S;
+        const int x = g & 1;
+        mbar_wait(BAR(kBarQFull + s), static_cast<uint32_t>((g / S) & 1));
+        tc_fence_after();
+        TATN_EV2(g, 2);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t offa = voff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128 + 64, dKV0 + (offa >> 4), dDOk0 + ((s * Cfg::kQTile + offb) >> 4),
+                 idesc_s, kk > 0 ? 1u : 0u);
+        }
+      };
+      auto front_s = [&](int g, uint32_t koff) {  // S^T = K Q^T  -> X cols [0,64)
+        const int s = g % S;
+        const int x = g & 1;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t offa = koff + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t offb = (kk >> 2) * Cfg::kQSub + (kk & 3) * 32;
+          mma_ss(tmem_base + Cfg::kTmemX + x * 128, dKV0 + (offa >> 4), dQk0 + ((s * Cfg::kQTile + offb) >> 4), idesc_s,
+                 kk > 0 ? 1u : 0u);
+        }
+        mma_commit(BAR(kBarSFull + x));
+        TATN_EV(g, 3);
+      };
+      // back(g): dV += P^T dO, dK += dS^T Q (A from TMEM), then dQ^T = K^T dS^T
+      // The previous item's dK / dV drained out of TMEM (once per item, empty items included: each
+      // AccFree phase is waited on in turn, so the Final commits below can never run two phases
+      // ahead of the dQ warpgroup that waits on them — with the issuers racing through empty
+      // items that aliased a parity and left the last epilogue waiting forever)
+      auto wait_acc_free = [&](int n) {
+        if (n > 0) {
+          mbar_wait(BAR(kBarAccFree), static_cast<uint32_t>((n - 1) & 1));
+          tc_fence_after();
+        }
+      };
+      auto back = [&](int g, int i, int n, uint32_t koff) {
+        const int x = g & 1;
+        const int s = g % S;
+        mbar_wait(BAR(kBarPFull + x), static_cast<uint32_t>((g >> 1) & 1));
+        tc_fence_after();
+        TATN_EV(g, 2);
+        if (i == 2 && n == 0) TATN_TRACE_AT(11);
+        const uint32_t accf = i > 0 ? 1u : 0u;
+        // P^T, dS^T (16-bit): PdS_x cols [0,32) / [32,64)
+        const uint32_t tP = tmem_base + Cfg::kTmemPdS + x * 64;
+        const uint32_t tDS = tP + 32;
+#pragma unroll
+        for (int kk = 0; kk < kBwdQT / 16; ++kk)  // dV += P^T dO   (dO MN-major, 16 queries per step)
+          mma_ts(tmem_base + Cfg::kTmemDV, tP + kk * 8, dDOmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc,
+                 accf | (kk > 0 ? 1u : 0u));
+#pragma unroll
+        for (int kk = 0; kk < kBwdQT / 16; ++kk)  // dK += dS^T Q
+          mma_ts(tmem_base + Cfg::kTmemDK, tDS + kk * 8, dQmn0 + ((s * Cfg::kQTile + kk * 2048) >> 4), idesc_acc,
+                 accf | (kk > 0 ? 1u : 0u));
+        // Q_i / dO_i are done with (front(g) completed before S^T reached the softmax; the tile's
+        // lse2 / D were read by the softmax before PFull)
+        mma_commit(BAR(kBarQEmpty + s));
+        TATN_EV2(g, 5);
+        // dQ^T into PdS_x (after dV / dK have read it: in-order pipe)
+#pragma unroll
+        for (int kk = 0; kk < kBwdKT / 16; ++kk)
+          mma_ss(tP, dKmn0 + ((koff + kk * 2048) >> 4), dDS0 + (((g % Cfg::kDSBufs) * Cfg::kDSBytes + kk * 2048) >> 4), idesc_dq,
+                 kk > 0 ? 1u : 0u);
+        mma_commit(BAR(kBarDQFull + x));
+        mma_commit(BAR(kBarDSEmpty + g % Cfg::kDSBufs));
+        TATN_EV(g, 4);
+      };
+      int g0 = 0;  // Q tiles issued before the current item
+      int w_next = take_item_1(0);
+      for (int n = 0; w_next >= 0; ++n) {
+        const int w = w_next;
+        const int cnt = item(w, n).cnt;
+        const int kb = n % NKV;
+        const uint32_t koff = static_cast<uint32_t>(kb * 2 * Cfg::kKVTile);  // K of buffer kb
+        const uint32_t voff = koff + Cfg::kKVTile;
+        if (fronts) TATN_EVI(n, 2);  // MMA warp starts the item (item taken)
+        mbar_wait(BAR(kBarKVFull + kb), static_cast<uint32_t>((n / NKV) & 1));
+        if (fronts) TATN_EVI(n, 3);  // K / V landed
+        tc_fence_after();
+        if (fronts && n == 0) TATN_TRACE_AT(1);
+#ifdef TATN_TRACE
+        if (fronts && n == 0 && g_tatn_trace) g_tatn_trace[static_cast<size_t>(blockIdx.x) * 16 + 6] = cnt;
+#endif
+        if (fronts) {
+          // front(g) as soon as the softmax holds S^T / dP^T of tile g - 2 (same X buffer) in registers
+          for (int i = 0; i < cnt; ++i) {
+            const int g = g0 + i;
+            TATN_EV2(g, 0);
+            if (g >= 2) {
+              mbar_wait(BAR(kBarXFree + (g & 1)), static_cast<uint32_t>(((g >> 1) & 1) ^ 1));
+              tc_fence_after();
+            }
+            TATN_EV2(g, 1);
+            front_dp(g, voff);
+            front_s(g, koff);
+          }
+        } else {
+          wait_acc_free(n);
+          for (int i = 0; i < cnt; ++i) back(g0 + i, i, n, koff);
+          mma_commit(BAR(kBarFinal));
+        }
+        mma_commit(BAR(kBarKVFree + kb));  // one of two arrivals
+        w_next = take_item_1(n + 1);
+        g0 += cnt;
+      }
+    }
+    __syncwarp();
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax warpgroups
     // warpgroup sg takes the Q tiles of parity sg (ping-pong over the two X buffers)
@@ -732,6 +877,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int s = g % S;
         const int x = g & 1;  // X buffer (== sg)
         const uint32_t tX = tmem_base + lane_off + Cfg::kTmemX + x * 128;
+        // P^T, dS^T (16-bit): PdS_x cols [0,32) / [32,64) at d = 64, else over S^T / dP^T in X_x
+        const uint32_t tP = Cfg::kEarlyX ? tmem_base + lane_off + Cfg::kTmemPdS + x * 64 : tX;
+        const uint32_t tDS = tP + (Cfg::kEarlyX ? 32 : 64);
         if (p.visited != nullptr && r == 0) {
           const long long bit = static_cast<long long>(i >> 1) * p.tc + it.j;
           atomicOr(p.visited + (bit >> 5), 1u << (bit & 31));
@@ -818,12 +966,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
               }
             }
+            if (r == 0) TATN_EV2(g, half == 0 ? 3 : 6);  // half computed
             if (half == 0) {
               tmem_ld32_async(tX + 32, sr);
               tmem_ld32_async(tX + 96, dp);
+              if constexpr (Cfg::kEarlyX) {
+                // all of S^T / dP^T in registers: X_x may take the front of tile g + 2
+                tmem_ld_wait32(sr);
+                tmem_ld_wait32(dp);
+                tc_fence_before();
+                mbar_arrive(BAR(kBarXFree + x));
+                if (r == 0) TATN_EV2(g, 7);
+                // PdS_x: dQ^T(g - 2) read out by the dQ warpgroup
+                mbar_wait(BAR(kBarDQEmpty + x), static_cast<uint32_t>(((g >> 1) & 1) ^ 1));
+                tc_fence_after();
+                if (r == 0) TATN_EV2(g, 4);
+              }
             }
-            tmem_st16(tX + half * 16, pk);       // P^T   -> X cols [0,32)
-            tmem_st16(tX + 64 + half * 16, dk);  // dS^T  -> X cols [64,96)
+            tmem_st16(tP + half * 16, pk);   // P^T
+            tmem_st16(tDS + half * 16, dk);  // dS^T
             if (half == 0) {
               // the dQ^T MMA of tile g - 2 must have released the dS^T buffer, and in a new
               // item the previous item's dK / dV staging must have been stored
@@ -837,7 +998,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               const int chunk = half * 4 + cc;
               st_shared_v4(drow + ((chunk ^ (r & 7)) << 4), dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
             }
-            if (half == 0) {
+            if (!Cfg::kEarlyX && half == 0) {
               tmem_ld_wait32(sr);
               tmem_ld_wait32(dp);
             }
@@ -881,7 +1042,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (row == 0 && g == 2) TATN_TRACE_AT(12);
         uint32_t v[64];
         if (Cfg::kDQ64 || active) {  // warp-uniform: tcgen05.ld is .sync.aligned
-          const uint32_t tX = tmem_base + lane_off + (Cfg::kSepDQ ? Cfg::kTmemDQ + x * 64 : Cfg::kTmemX + x * 128);
+          const uint32_t tX = tmem_base + lane_off + (Cfg::kEarlyX ? Cfg::kTmemPdS + x * 64 : Cfg::kTmemX + x * 128);
           tmem_ld32(tX, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
           tmem_ld32(tX + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
         }
@@ -1147,7 +1308,7 @@ static cudaError_t tatn_bwd_launch_t(const tatn_attn_desc& d, const void* q, con
                                        ? p.n_items
                                        : std::min(p.n_items, n_sm)));
   cudaEvent_t prof_stop = tatn_host::profile_begin(1, stream);
-  cudaError_t e = tatn_host::launch(kern, grid, dim3(tatn_dev::kBwdThreads), Cfg::kSmemBytes, stream, mq, mk, mv, mdo,
+  cudaError_t e = tatn_host::launch(kern, grid, dim3(Cfg::kThreads), Cfg::kSmemBytes, stream, mq, mk, mv, mdo,
                                     mdk, mdv, p, static_cast<const float*>(lse2), Nq_pad);
   if (prof_stop) cudaEventRecord(prof_stop, stream);
   if (e != cudaSuccess) return e;

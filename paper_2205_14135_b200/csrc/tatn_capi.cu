@@ -375,6 +375,14 @@ int tatn_merge_partials(int32_t R, int32_t B, int32_t H, int32_t Nq, int32_t d, 
 
 int tatn_last_launch_count(void) { return g_last_launches; }
 
+#ifdef TATN_WAIT_DEBUG
+// debug builds only: where a deadlocked mbarrier wait was stuck (scripts/repro_tiny.py)
+int tatn_debug_set_wait_dbg(void* dev_buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  return cudaMemcpyToSymbol(tatn_dev::g_tatn_wait_dbg, &p, sizeof(p)) == cudaSuccess ? TATN_OK : TATN_E_CUDA;
+}
+#endif
+
 #ifdef TATN_TRACE
 // debug builds only: per-CTA globaltimer trace of the forward kernel (scripts/trace_fwd.py)
 int tatn_debug_set_trace(void* dev_buf) {

@@ -256,18 +256,17 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
       }
       return next_item(ps);
     };
-    // Every item (also one without tiles) completes one QFull phase of buffer n & 1; they are
-    // waited strictly in item order, so a parity wait is never two phases ahead of its barrier.
-    int q_waited = -1;
-    auto sync_q = [&](int upto) {
-      for (int i = q_waited + 1; i <= upto; ++i)
-        mbar_wait(BAR(kBarQFull + (i & 1)), static_cast<uint32_t>((i >> 1) & 1));
-      if (upto > q_waited) q_waited = upto;
-    };
+    // Every item (also one without tiles) completes one QFull phase of buffer n & 1. The MMA
+    // warp waits only for the items it has tiles of, directly on item n's phase: Q(n + 2) is
+    // loaded into the same buffer only after item n's epilogue (which needs this warp's PVs) and
+    // Q(n) only after item n - 2's, so when the wait is issued the barrier is exactly at phase
+    // n >> 1 or one before it. (Waiting the skipped items' phases later, in order, as round 1 did,
+    // aliased parities once the softmax warpgroup had run the producer two or more phases ahead
+    // through items without tiles — all-padded batches deadlocked.)
     auto issue_qk = [&](const Pos& ps, int g) {
       const int stage = g & 1;
       const int qb = ps.n & 1;
-      if (ps.first) sync_q(ps.n);
+      if (ps.first) mbar_wait(BAR(kBarQFull + qb), static_cast<uint32_t>((ps.n >> 1) & 1));
       mbar_wait(BAR(kBarKFull + stage), static_cast<uint32_t>((g >> 1) & 1));
       tc_fence_after();
       if (elect_one_sync()) {
@@ -334,7 +333,6 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
         ++g;
       }
     }
-    sync_q(n_taken - 1);  // trailing items without tiles: consume their QFull phases
   } else if (warp < 4) {
     // ------------------------------------------------------------ softmax + epilogue warpgroup
     const int row = warp * 32 + lane;  // row within the tile == TMEM lane

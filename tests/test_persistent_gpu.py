@@ -63,6 +63,21 @@ def test_many_tiny_items_and_empty_items(cuda_device, d):
     assert np.all(got["dk"][empty] == 0) and np.all(got["dq"][empty] == 0)
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_every_item_without_keys(cuda_device, d):
+    # every batch fully padded: no (b, h, tile) item has a key tile. The issuers run through empty
+    # items while the softmax / epilogue roles keep pace, which deadlocked two bugs: the d = 64
+    # forward's MMA warp waited the skipped items' QFull phases late (aliased parities), and the
+    # backward's Final commits could run two phases ahead of the epilogue waiting on them.
+    B, H, N = 16, 40, 96
+    q, k, v, do = G.make_inputs(B, H, N, N, d, "fp16")
+    vl = np.zeros(B, dtype=np.int32)
+    got = G.run_gpu(q, k, v, do, "fp16", mask="key_padding", valid_len=vl)
+    assert np.all(got["o"] == 0) and np.all(np.isneginf(got["lse"]))
+    for key in ("dq", "dk", "dv"):
+        assert np.all(got[key] == 0), key
+
+
 def test_graph_replay_matches_eager(cuda_device):
     q, k, v, do = _inputs(8, 12, 1024, 64)
     spec = A.AttnSpec(mask="causal")
