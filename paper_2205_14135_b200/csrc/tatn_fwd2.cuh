@@ -35,7 +35,6 @@ struct Fwd2Cfg {
   static constexpr uint32_t kTmemO = 256;       // O_A, O_B
   static constexpr uint32_t kTmemP = 0;
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr bool kSeparateP = false;
 };
 
 // item w -> (bh, pair): head groups, heaviest causal pairs first within a group
@@ -405,72 +404,6 @@ __global__ void __launch_bounds__(384, 1)
             }
           }
         };
-        // One streaming pass over S: p = 2^(s*scale_log2 - m_use) per 32-column chunk
-        // (FFMA2 scale, MUFU ex2 or the FMA-pipe polynomial for (i & 7) < kEmuPairs on
-        // full tiles), P (16-bit) to TMEM at tP, row sum in FP32x2; optionally tracks
-        // the raw row max. With aliased P (tP == tS) chunk c lands on S columns
-        // [16c, 16c+16), which the pass has already consumed.
-        auto exp_pass = [&](float m_use, float& raw_max) -> float {
-          const uint64_t negm = f2_pack(-m_use, -m_use);
-          uint64_t rsum0 = f2_pack(0.f, 0.f), rsum1 = rsum0;
-          float mx0 = -INFINITY, mx1 = -INFINITY;
-          uint32_t ra[32], rb[32];
-          tmem_ld32_async(tS, ra);
-          tmem_ld_wait32(ra);
-  #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t (&r)[32] = (c & 1) ? rb : ra;
-            uint32_t (&nxt)[32] = (c & 1) ? ra : rb;
-            if (c + 1 < 4) tmem_ld32_async(tS + (c + 1) * 32, nxt);
-            apply_mask(r, c);
-            if (Cfg::kSeparateP) {
-  #pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                mx0 = fmax3(mx0, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
-                mx1 = fmax3(mx1, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
-              }
-            }
-            uint32_t pk[16];
-            // straight-line bodies: the polynomial pairs interleave with the MUFU pairs
-            auto exp_chunk = [&](auto emu_on) {
-              constexpr bool kEmu = decltype(emu_on)::value;
-  #pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const int i = c * 16 + k;
-                const uint64_t x =
-                    f2_fma(f2_pack(__uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1])), sl2x2, negm);
-                uint64_t pv;
-                if (kEmu && (i & 7) < kEmuPairsD<D>) {
-                  pv = exp2_poly_f2(x);
-                } else {
-                  float x0, x1;
-                  f2_unpack(x, x0, x1);
-                  pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
-                }
-                float p0, p1;
-                f2_unpack(pv, p0, p1);
-                if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
-                  const int j0 = p.k_off + k0 + c * 32 + 2 * k;  // global key index
-                  p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
-                  p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
-                }
-                pk[k] = pack2<BF16>(p0, p1);
-                if (k & 1) rsum1 = f2_add(rsum1, pv);
-                else rsum0 = f2_add(rsum0, pv);
-              }
-            };
-            // the polynomial needs finite x: full tiles with m_use <= the true max + threshold
-            if (kEmuPairsD<D> > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
-            else exp_chunk(std::false_type{});
-            tmem_st16(tP + c * 16, pk);
-            if (c + 1 < 4) tmem_ld_wait32(nxt);
-          }
-          raw_max = fmaxf(mx0, mx1);
-          float rs0, rs1, rs2, rs3;
-          f2_unpack(rsum0, rs0, rs1);
-          f2_unpack(rsum1, rs2, rs3);
-          return (rs0 + rs1) + (rs2 + rs3);
-        };
         auto rescale_o = [&](float alpha, bool mine) {
           if (__any_sync(0xffffffffu, mine)) {
   #pragma unroll
@@ -484,61 +417,74 @@ __global__ void __launch_bounds__(384, 1)
           }
         };
         float row_sum = 0.f;
-        bool settled = false;
-        if (Cfg::kSeparateP && n_done > 0 && __all_sync(0xffffffffu, m_run != -INFINITY)) {
-          // optimistic single pass against the running max; redo only if the max jumped
-          // past the lazy-rescale threshold (the polynomial clamps overflowing inputs, and
-          // such a pass is discarded)
-          float raw_max;
-          row_sum = exp_pass(m_run, raw_max);
-          const float m_tile = raw_max * sl2;
-          const bool jumped = m_tile - m_run > kRescaleThreshold;
-          settled = !__any_sync(0xffffffffu, jumped);
-          if (!settled) {  // warp-uniform branch: TMEM ld/st below are .sync.aligned
-            float alpha = 1.f;
-            if (jumped) {
-              alpha = ex2_approx(m_run - m_tile);
-              m_run = m_tile;
-              l_run *= alpha;
-            }
-            rescale_o(alpha, jumped);
+        // one pass: all of S(t) in registers (128 of the warpgroup's 208), then the row max, the
+        // lazy rescale and the exponentials from registers; P (16-bit) overwrites S columns
+        // [16c, 16c + 16) in TMEM, all of which are already in registers. One TMEM read of the
+        // 64 KB tile instead of two (row max pass + exponential pass).
+        uint32_t sv[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32_async(tS + c * 32, sv[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_wait32(sv[c]);
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          apply_mask(sv[c], c);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            mx0 = fmax3(mx0, __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
+            mx1 = fmax3(mx1, __uint_as_float(sv[c][i + 2]), __uint_as_float(sv[c][i + 3]));
           }
         }
-        if (!settled) {
-          float m_tile;
-          if (Cfg::kSeparateP && n_done > 0 && __all_sync(0xffffffffu, m_run != -INFINITY)) {
-            m_tile = m_run;  // already advanced above
-          } else {
-            // pass 1: row max, streaming S from TMEM in 32-column chunks (3-input max)
-            float mx0 = -INFINITY, mx1 = -INFINITY;
-            uint32_t ra[32], rb[32];
-            tmem_ld32_async(tS, ra);
-            tmem_ld_wait32(ra);
-  #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t (&cur)[32] = (c & 1) ? rb : ra;
-              uint32_t (&nxt)[32] = (c & 1) ? ra : rb;
-              if (c + 1 < 4) tmem_ld32_async(tS + (c + 1) * 32, nxt);
-              apply_mask(cur, c);
-  #pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                mx0 = fmax3(mx0, __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]));
-                mx1 = fmax3(mx1, __uint_as_float(cur[i + 2]), __uint_as_float(cur[i + 3]));
+        const float m_tile = fmaxf(mx0, mx1) * sl2;
+        float alpha = 1.f;
+        if (m_tile - m_run > kRescaleThreshold) {  // false for NaN (both -inf)
+          alpha = ex2_approx(m_run - m_tile);      // 0 when m_run == -inf
+          m_run = m_tile;
+        }
+        l_run *= alpha;
+        rescale_o(alpha, (n_done > 0) && (alpha != 1.f));
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        const uint64_t negm = f2_pack(-m_use, -m_use);
+        uint64_t rsum0 = f2_pack(0.f, 0.f), rsum1 = rsum0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+          auto exp_chunk = [&](auto emu_on) {
+            constexpr bool kEmu = decltype(emu_on)::value;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int i = c * 16 + k;
+              const uint64_t x =
+                  f2_fma(f2_pack(__uint_as_float(sv[c][2 * k]), __uint_as_float(sv[c][2 * k + 1])), sl2x2, negm);
+              uint64_t pv;
+              if (kEmu && (i & 7) < kEmuPairsD<D>) {
+                pv = exp2_poly_f2(x);
+              } else {
+                float x0, x1;
+                f2_unpack(x, x0, x1);
+                pv = f2_pack(ex2_approx(x0), ex2_approx(x1));
               }
-              if (c + 1 < 4) tmem_ld_wait32(nxt);
+              float p0, p1;
+              f2_unpack(pv, p0, p1);
+              if constexpr (DROP) {  // the MMA takes P * Z / (1 - p); l keeps the undropped P
+                const int j0 = p.k_off + k0 + c * 32 + 2 * k;  // global key index
+                p0 = drop_keep(drow, j0, p.drop_thresh) ? p0 * p.drop_scale : 0.f;
+                p1 = drop_keep(drow, j0 + 1, p.drop_thresh) ? p1 * p.drop_scale : 0.f;
+              }
+              pk[k] = pack2<BF16>(p0, p1);
+              if (k & 1) rsum1 = f2_add(rsum1, pv);
+              else rsum0 = f2_add(rsum0, pv);
             }
-            m_tile = fmaxf(mx0, mx1) * sl2;
-            float alpha = 1.f;
-            if (m_tile - m_run > kRescaleThreshold) {  // false for NaN (both -inf)
-              alpha = ex2_approx(m_run - m_tile);      // 0 when m_run == -inf
-              m_run = m_tile;
-            }
-            l_run *= alpha;
-            rescale_o(alpha, (n_done > 0) && (alpha != 1.f));
-          }
-          float unused;
-          row_sum = exp_pass((m_run == -INFINITY) ? 0.f : m_run, unused);
+          };
+          if (kEmuPairsD<D> > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
+          else exp_chunk(std::false_type{});
+          tmem_st16(tP + c * 16, pk);
         }
+        float rs0, rs1, rs2, rs3;
+        f2_unpack(rsum0, rs0, rs1);
+        f2_unpack(rsum1, rs2, rs3);
+        row_sum = (rs0 + rs1) + (rs2 + rs3);
         l_run += row_sum;
         tmem_st_wait();
         tc_fence_before();
