@@ -28,10 +28,13 @@ constexpr float kRescaleThreshold = 8.0f;  // lazy O rescale (log2 units)
 #define TATN_EMU_PAIRS 1
 #endif
 constexpr int kEmuPairs = TATN_EMU_PAIRS;
+#ifndef TATN_EMU_PAIRS_D128
+#define TATN_EMU_PAIRS_D128 0  // d = 128 forward: exp2 pairs (of 8) on the FMA pipe
+#endif
 // d = 128 keeps every exp2 on MUFU: there the MMA and MUFU are balanced and the FMA-pipe
 // polynomial measured slower (N = 8K causal fwd 889 -> 912 TFLOP/s without it)
 template <int D>
-constexpr int kEmuPairsD = D == 128 ? 0 : kEmuPairs;
+constexpr int kEmuPairsD = D == 128 ? TATN_EMU_PAIRS_D128 : kEmuPairs;
 
 // ---------------------------------------------------------------- partial-result merge
 // merge_stats (softmax.cpp:62-83) in log form over R key shards; one thread per 8 elements
