@@ -104,8 +104,9 @@ __global__ void __launch_bounds__(384, 1)
   const int kBarOFinal = kBarPFull + 2;  // [2]
   const int kBarItem = kBarOFinal + 2;   // [kRing]
   const int kBarItemFree = kBarItem + Cfg::kRing;
-  const int kNumBars = kBarItemFree + Cfg::kRing;
-  static_assert(8 * (4 * S + 8 + 2 * Cfg::kRing) <= 8 * 30, "barrier region");
+  const int kBarPHalf = kBarItemFree + Cfg::kRing;  // [2] P columns [0, 32) (keys 0-63) written
+  const int kNumBars = kBarPHalf + 2;
+  static_assert(8 * (4 * S + 10 + 2 * Cfg::kRing) <= 8 * 30, "barrier region");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffBar + 8 * 30);
   volatile int* ring = reinterpret_cast<volatile int*>(smem_gen + Cfg::kOffRing);
   uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
@@ -117,6 +118,8 @@ __global__ void __launch_bounds__(384, 1)
     for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
     mbar_init(BAR(kBarPFull + 0), 128);
     mbar_init(BAR(kBarPFull + 1), 128);
+    mbar_init(BAR(kBarPHalf + 0), 128);
+    mbar_init(BAR(kBarPHalf + 1), 128);
     for (int k = 0; k < Cfg::kRing; ++k) mbar_init(BAR(kBarItemFree + k), 9);  // MMA warp + 8 softmax warps
     fence_mbar_init();
   }
@@ -297,14 +300,25 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         for (int q = 0; q < 2; ++q) {
           if (!sc.member(q, t)) continue;
+          // P·V in two halves: keys 0-63 as soon as the softmax has written their P (PHalf), under
+          // its exponentials of keys 64-127
+          mbar_wait(BAR(kBarPHalf + q), pph[q]);
+          tc_fence_after();
+          if (elect_one_sync()) {
+#pragma unroll
+            for (int kk = 0; kk < kBN / 32; ++kk)
+              mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemP + q * 128 + kk * 8,
+                     vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv, (acc[q] | (kk > 0 ? 1u : 0u)));
+          }
+          __syncwarp();
           mbar_wait(BAR(kBarPFull + q), pph[q]);
           pph[q] ^= 1;
           tc_fence_after();
           if (elect_one_sync()) {
 #pragma unroll
-            for (int kk = 0; kk < kBN / 16; ++kk)
+            for (int kk = kBN / 32; kk < kBN / 16; ++kk)
               mma_ts(tmem_base + Cfg::kTmemO + q * D, tmem_base + Cfg::kTmemP + q * 128 + kk * 8,
-                     vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv, (acc[q] | (kk > 0 ? 1u : 0u)));
+                     vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv, 1u);
             if (!sc.has_after(q, t)) mma_commit(BAR(kBarOFinal + q));  // tile q's O is final
           }
           __syncwarp();
@@ -480,6 +494,11 @@ __global__ void __launch_bounds__(384, 1)
           if (kEmuPairsD<D> > 0 && !need_mask && !DROP) exp_chunk(std::true_type{});
           else exp_chunk(std::false_type{});
           tmem_st16(tP + c * 16, pk);
+          if (c == 1) {  // P of keys 0-63 in TMEM: the first half of P·V may start
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(BAR(kBarPHalf + q));
+          }
         }
         float rs0, rs1, rs2, rs3;
         f2_unpack(rsum0, rs0, rs1);
