@@ -69,8 +69,9 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
   const int kBarQFull = 8, kBarQFree = 10;                                 // [2] each (Q buffer)
   const int kBarSFull = 12, kBarSFree = 13, kBarPFull = 14, kBarPVDone = 15, kBarOFinal = 16;
   const int kBarItem = 17, kBarItemFree = kBarItem + Cfg::kRing;  // [kRing] each
-  const int kNumBars = kBarItemFree + Cfg::kRing;
-  static_assert(8 * (17 + 2 * Cfg::kRing) <= 8 * 28, "barrier region");
+  const int kBarPHalf = kBarItemFree + Cfg::kRing;  // P of keys 0-63 written
+  const int kNumBars = kBarPHalf + 1;
+  static_assert(8 * (18 + 2 * Cfg::kRing) <= 8 * 28, "barrier region");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffBar + 8 * 28);
   volatile int* ring = reinterpret_cast<volatile int*>(smem_gen + Cfg::kOffRing);
   uint32_t* mask_smem = reinterpret_cast<uint32_t*>(smem_gen + Cfg::kOffMask);
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
     for (int i = 0; i < kNumBars; ++i) mbar_init(BAR(i), 1);
     mbar_init(BAR(kBarSFree), 128);
     mbar_init(BAR(kBarPFull), 128);
+    mbar_init(BAR(kBarPHalf), 128);
     for (int b = 0; b < 2; ++b) mbar_init(BAR(kBarQFree + b), 128);  // O staged by every softmax thread
     for (int k = 0; k < Cfg::kRing; ++k) mbar_init(BAR(kBarItemFree + k), 5);  // MMA warp + 4 softmax warps
     fence_mbar_init();
@@ -283,18 +285,29 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
       }
       __syncwarp();
     };
+    // P·V in two halves: keys 0-63 once the softmax has written their P (PHalf), under its
+    // exponentials of keys 64-127, then keys 64-127 after PFull
     auto issue_pv = [&](const Pos& ps, int g, bool last_of_item) {
-      mbar_wait(BAR(kBarPFull), static_cast<uint32_t>(g & 1));
-      if (lane == 0) TATN_EV(g, 3);
       const int stage = g & 1;
+      mbar_wait(BAR(kBarPHalf), static_cast<uint32_t>(g & 1));
       mbar_wait(BAR(kBarVFull + stage), static_cast<uint32_t>((g >> 1) & 1));
       tc_fence_after();
       if (elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
+        for (int kk = 0; kk < kBN / 32; ++kk)
           mma_ts(tmem_base + Cfg::kTmemO, tmem_base + Cfg::kTmemP + kk * 8,
                  vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv,
                  (ps.first ? 0u : 1u) | (kk > 0 ? 1u : 0u));
+      }
+      __syncwarp();
+      mbar_wait(BAR(kBarPFull), static_cast<uint32_t>(g & 1));
+      if (lane == 0) TATN_EV(g, 3);
+      tc_fence_after();
+      if (elect_one_sync()) {
+#pragma unroll
+        for (int kk = kBN / 32; kk < kBN / 16; ++kk)
+          mma_ts(tmem_base + Cfg::kTmemO, tmem_base + Cfg::kTmemP + kk * 8,
+                 vdesc0 + ((stage * Cfg::kTileBytes + kk * 2048) >> 4), idesc_pv, 1u);
         mma_commit(BAR(kBarPVDone));
         mma_commit(BAR(kBarVEmpty + stage));
         if (last_of_item) mma_commit(BAR(kBarOFinal));
@@ -471,6 +484,11 @@ __global__ void __launch_bounds__(kFwd1Threads, 2)
             }
             if (c == 0 && !pv_ready) wait_pv();  // PV(g-1) has read P(g-1)
             tmem_st16(tP + c * 16, pk);
+            if (c == 1) {  // P of keys 0-63 in TMEM: the first half of P·V may start
+              tmem_st_wait();
+              tc_fence_before();
+              mbar_arrive(BAR(kBarPHalf));
+            }
           }
           float rs0, rs1, rs2, rs3;
           f2_unpack(rsum0, rs0, rs1);
